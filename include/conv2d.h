@@ -1,0 +1,152 @@
+/*
+ * conv2d.h -- C-ABI of libconv2d.so: fp32 NHWC 2D-convolution forward on B200 (sm_100a).
+ *
+ * The operation (every algorithm below computes it; "a variety
+ * of different algorithms which all provide the same numeric results"):
+ *
+ *   y[n,ho,wo,f] = sum_{kh,kw,c} x[n, ho*Sr + kh - pad_top, wo*Sc + kw - pad_left, c] * w[kh,kw,c,f]
+ *
+ * out-of-bounds x reads as 0; cross-correlation (no filter flip).  Parameter
+ * space = SYCL-DNN's (Fig. 1 tuple "window size, stride, image
+ * rows, image columns, input features, output features", plus batch and
+ * SAME/VALID padding -- SPEC.md:40-45).  Shapes follow SPEC.md:48-56:
+ *   SAME : Ho = ceil(H/S);   VALID: Ho = floor((H-K)/S)+1, requires K <= H
+ *   pad_total = max((Ho-1)*S + K - H, 0); pad_top = floor(pad_total/2); pad_bottom = rest.
+ *
+ * Layouts (all dense, row-major, 64-bit indexed):
+ *   in   : NHWC  fp32, N*H*W*C elements
+ *   filt : HWCF  fp32 (Kh, Kw, C, F) -- i.e. a (Kh*Kw*C) x F row-major matrix
+ *   out  : N,Ho,Wo,F fp32
+ *
+ * Ownership: the caller owns every buffer; all pointers passed to
+ * conv2d_forward are DEVICE pointers, 16-byte aligned, and must not alias
+ * (in/filt are read-only, out and ws are written).  The library never
+ * allocates or frees device memory, and keeps no pointer after a call returns.
+ *
+ * Execution: conv2d_forward is stream-ordered and asynchronous on `stream`
+ * (a cudaStream_t; NULL = legacy default stream).  Parameter errors are
+ * returned synchronously before anything is launched.  Kernel launch errors
+ * are returned as CONV2D_ERR_CUDA (detail in conv2d_last_error()).  Results
+ * are bitwise reproducible for a fixed (params, algo, device): no atomics,
+ * split-K partial sums are reduced in a fixed order.
+ *
+ * Thread safety: every function may be called concurrently from several host
+ * threads; the auto-selector cache is mutex-protected.
+ */
+#ifndef CONV2D_B200_H
+#define CONV2D_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { CONV2D_PAD_SAME = 0, CONV2D_PAD_VALID = 1 } conv2d_padding_t;
+
+/* Math mode of the tensor-core paths.
+ *  FP32: fp32-faithful.  Tensor paths run 3xTF32 (a = a_hi + a_lo split;
+ *        a_hi*b_hi + a_hi*b_lo + a_lo*b_hi, fp32 accumulation); CUDA-core paths
+ *        run plain fp32 FFMA.  Tolerance max|err|/sum|x||w| <= 1e-5 (north_star).
+ *  TF32: one TF32 MMA per product (reported separately; tolerance 2e-3).
+ *        CUDA-core algorithms (direct, tiled) ignore it and stay exact fp32. */
+typedef enum { CONV2D_MATH_FP32 = 0, CONV2D_MATH_TF32 = 1 } conv2d_math_t;
+
+/* Algorithms.  Enum order is the auto-selector's tie-break order. */
+typedef enum {
+  CONV2D_ALGO_AUTO = 0,              /* measured-time argmin over supported algorithms, cached */
+  CONV2D_ALGO_DIRECT = 1,            /* one thread per output vector, FFMA */
+  CONV2D_ALGO_TILED = 2,             /* CTA output tile, smem halo, register blocking */
+  CONV2D_ALGO_IMPLICIT_GEMM = 3,     /* tcgen05/TMEM GEMM over the never-materialised im2col matrix */
+  CONV2D_ALGO_WINOGRAD_F2X2_3X3 = 4, /* Winograd F(2x2,3x3), tensor-core batched GEMM */
+  CONV2D_ALGO_MATMUL_1X1 = 5         /* 1x1/stride-1 conv as one GEMM */
+} conv2d_algo_t;
+#define CONV2D_NUM_ALGOS 6
+
+typedef struct {
+  int32_t batch, in_rows, in_cols, channels, features;
+  int32_t window_rows, window_cols, stride_rows, stride_cols;
+  conv2d_padding_t padding;
+  conv2d_math_t math;
+} conv2d_params_t;
+
+typedef enum {
+  CONV2D_OK = 0,
+  CONV2D_ERR_INVALID_PARAMS = 1, /* dim < 1, bad enum, VALID with K > H, element count overflow */
+  CONV2D_ERR_UNSUPPORTED = 2,    /* algorithm incompatible with params (never silently replaced) */
+  CONV2D_ERR_WORKSPACE = 3,      /* ws NULL or ws_bytes < conv2d_query_workspace() */
+  CONV2D_ERR_ALIGNMENT = 4,      /* a device pointer is not 16-byte aligned */
+  CONV2D_ERR_NULL = 5,           /* a required pointer argument is NULL */
+  CONV2D_ERR_CUDA = 6,           /* a CUDA call failed; see conv2d_last_error() */
+  CONV2D_ERR_NO_DEVICE = 7       /* no sm_100 device is current */
+} conv2d_status_t;
+
+/* Shape inference (no device needed).  out_nhwf = {N, Ho, Wo, F};
+ * pads_tblr = {top, bottom, left, right} (either may be NULL). */
+conv2d_status_t conv2d_output_shape(const conv2d_params_t* p, int32_t out_nhwf[4], int32_t pads_tblr[4]);
+
+/* 2*N*Ho*Wo*Kh*Kw*C*F: direct-convolution flops, used for
+ * GFLOP/s of every algorithm including Winograd (reading R8). */
+conv2d_status_t conv2d_flop_count(const conv2d_params_t* p, uint64_t* flops);
+
+/* *supported = 1 iff `algo` can run `p` (no device needed).  AUTO is always supported.
+ *   DIRECT, TILED, IMPLICIT_GEMM : every valid params
+ *   MATMUL_1X1                   : Kh = Kw = 1 and Sr = Sc = 1
+ *   WINOGRAD_F2X2_3X3            : Kh = Kw = 3, Sr = Sc = 1, C >= 32 (reading R13/R16) */
+conv2d_status_t conv2d_supports(const conv2d_params_t* p, conv2d_algo_t algo, int* supported);
+
+/* Device workspace bytes `algo` needs for `p` (AUTO: max over supported
+ * algorithms).  0 means ws may be NULL. */
+conv2d_status_t conv2d_query_workspace(const conv2d_params_t* p, conv2d_algo_t algo, size_t* bytes);
+
+/* The forward pass.  in/filt/out/ws: device pointers (see Ownership).
+ * ws_bytes must be >= conv2d_query_workspace(p, algo).  With AUTO on a cache
+ * miss this tunes first (see conv2d_autotune: it SYNCHRONISES the stream and
+ * uses out/ws as scratch), then runs the chosen algorithm. */
+conv2d_status_t conv2d_forward(const conv2d_params_t* p, conv2d_algo_t algo, const float* in,
+                               const float* filt, float* out, void* ws, size_t ws_bytes, void* stream);
+
+/* Auto-selector (PAPER.md:209-215 per-device algorithm choice):
+ * time every supported algorithm on the caller's buffers (CUDA events, W warm-ups
+ * then R reps, best-of-R), pick the argmin with ties broken by enum order, cache it
+ * under (params incl. batch/padding/math, device), and write it to *chosen.
+ * Synchronises `stream`.  ws must be sized for AUTO. */
+conv2d_status_t conv2d_autotune(const conv2d_params_t* p, const float* in, const float* filt, float* out,
+                                void* ws, size_t ws_bytes, void* stream, conv2d_algo_t* chosen);
+
+/* Cache query without tuning: CONV2D_OK and *chosen if cached, else
+ * CONV2D_ERR_UNSUPPORTED and *chosen = AUTO. */
+conv2d_status_t conv2d_selected(const conv2d_params_t* p, conv2d_algo_t* chosen);
+
+/* Seed the cache explicitly (e.g. to replay a choice broadcast from rank 0).
+ * Fails with CONV2D_ERR_UNSUPPORTED if `algo` cannot run `p`. */
+conv2d_status_t conv2d_set_selected(const conv2d_params_t* p, conv2d_algo_t algo);
+
+/* Drop every cached choice. */
+void conv2d_clear_selection_cache(void);
+
+/* Last per-algorithm best times (microseconds) from the most recent autotune on
+ * this thread; times[a] < 0 for algorithms not timed.  times must hold CONV2D_NUM_ALGOS. */
+void conv2d_last_tune_times(double times_us[CONV2D_NUM_ALGOS]);
+
+/* Number of kernel launches conv2d_forward(p, algo) issues (AUTO: of the cached choice,
+ * or -1 if not cached).  Used by bench.py to report gpu_launches. */
+int conv2d_launch_count(const conv2d_params_t* p, conv2d_algo_t algo);
+
+/* Counter-based seeded generator on the device (NOT part of the convolution;
+ * the device twin of paper_1904_04174_b200/synth.py, used to fill multi-GB bench
+ * inputs quickly).  Writes count floats, element i = gen(key, offset + i);
+ * dist 0 = uniform [-1,1), 1 = integers {-2..2}. */
+conv2d_status_t conv2d_synth_fill(float* dst, uint64_t count, uint64_t key, uint64_t offset, int dist,
+                                  void* stream);
+
+const char* conv2d_status_string(conv2d_status_t s);
+const char* conv2d_algo_name(conv2d_algo_t a);
+/* Thread-local detail of the last error on this thread ("" if none). */
+const char* conv2d_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CONV2D_B200_H */

@@ -1,0 +1,234 @@
+"""Python binding of libconv2d.so (include/conv2d.h) -- argument marshalling only.
+
+Every step of the convolution runs in the library's sm_100a kernels; this module
+only converts torch tensors to device pointers, picks up the current CUDA stream
+and raises on error codes.  There is no CPU or library fallback: if libconv2d.so
+is missing or fails to load, importing this module raises.
+
+Names mirror the C-ABI (conv2d_forward, conv2d_query_workspace, ...).  ``forward``
+is the convenience call a user makes: it allocates the output and workspace with
+torch and calls conv2d_forward on the current stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("CONV2D_LIB", os.path.join(_HERE, "libconv2d.so"))
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libconv2d.so not found at {LIB_PATH}: build it with "
+                      f"`python -m paper_1904_04174_b200.build` (no fallback path exists)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+PAD_SAME, PAD_VALID = 0, 1
+MATH_FP32, MATH_TF32 = 0, 1
+ALGO_AUTO, ALGO_DIRECT, ALGO_TILED, ALGO_IMPLICIT_GEMM, ALGO_WINOGRAD_F2X2_3X3, ALGO_MATMUL_1X1 = range(6)
+NUM_ALGOS = 6
+ALGO_NAMES = ["auto", "direct", "tiled", "implicit_gemm", "winograd_f2x2_3x3", "matmul_1x1"]
+ALGO_BY_NAME = {n: i for i, n in enumerate(ALGO_NAMES)}
+
+STATUS = ["CONV2D_OK", "CONV2D_ERR_INVALID_PARAMS", "CONV2D_ERR_UNSUPPORTED", "CONV2D_ERR_WORKSPACE",
+          "CONV2D_ERR_ALIGNMENT", "CONV2D_ERR_NULL", "CONV2D_ERR_CUDA", "CONV2D_ERR_NO_DEVICE"]
+OK, ERR_INVALID_PARAMS, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_ALIGNMENT, ERR_NULL, ERR_CUDA, ERR_NO_DEVICE = range(8)
+
+EXPORTED = ["conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv2d_query_workspace",
+            "conv2d_forward", "conv2d_autotune", "conv2d_selected", "conv2d_set_selected",
+            "conv2d_clear_selection_cache", "conv2d_last_tune_times", "conv2d_launch_count",
+            "conv2d_synth_fill", "conv2d_status_string", "conv2d_algo_name", "conv2d_last_error"]
+
+
+class conv2d_params_t(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "batch", "in_rows", "in_cols", "channels", "features",
+        "window_rows", "window_cols", "stride_rows", "stride_cols", "padding", "math")]
+
+
+class Conv2dError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        detail = _lib.conv2d_last_error().decode()
+        super().__init__(f"{where}: {STATUS[status] if 0 <= status < len(STATUS) else status}: {detail}")
+
+
+_P = ctypes.POINTER(conv2d_params_t)
+_vp = ctypes.c_void_p
+_lib.conv2d_output_shape.argtypes = [_P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+_lib.conv2d_flop_count.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64)]
+_lib.conv2d_supports.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+_lib.conv2d_query_workspace.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]
+_lib.conv2d_forward.argtypes = [_P, ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]
+_lib.conv2d_autotune.argtypes = [_P, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp, ctypes.POINTER(ctypes.c_int)]
+_lib.conv2d_selected.argtypes = [_P, ctypes.POINTER(ctypes.c_int)]
+_lib.conv2d_set_selected.argtypes = [_P, ctypes.c_int]
+_lib.conv2d_clear_selection_cache.argtypes = []
+_lib.conv2d_clear_selection_cache.restype = None
+_lib.conv2d_last_tune_times.argtypes = [ctypes.POINTER(ctypes.c_double)]
+_lib.conv2d_last_tune_times.restype = None
+_lib.conv2d_launch_count.argtypes = [_P, ctypes.c_int]
+_lib.conv2d_synth_fill.argtypes = [_vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, _vp]
+_lib.conv2d_status_string.argtypes = [ctypes.c_int]
+_lib.conv2d_status_string.restype = ctypes.c_char_p
+_lib.conv2d_algo_name.argtypes = [ctypes.c_int]
+_lib.conv2d_algo_name.restype = ctypes.c_char_p
+_lib.conv2d_last_error.argtypes = []
+_lib.conv2d_last_error.restype = ctypes.c_char_p
+for _f in ("conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv2d_query_workspace",
+           "conv2d_forward", "conv2d_autotune", "conv2d_selected", "conv2d_set_selected",
+           "conv2d_launch_count", "conv2d_synth_fill"):
+    getattr(_lib, _f).restype = ctypes.c_int
+
+
+@dataclass(frozen=True)
+class Params:
+    batch: int
+    in_rows: int
+    in_cols: int
+    channels: int
+    features: int
+    window_rows: int
+    window_cols: int
+    stride_rows: int = 1
+    stride_cols: int = 1
+    padding: int = PAD_SAME
+    math: int = MATH_FP32
+
+    def c(self) -> conv2d_params_t:
+        return conv2d_params_t(self.batch, self.in_rows, self.in_cols, self.channels, self.features,
+                               self.window_rows, self.window_cols, self.stride_rows, self.stride_cols,
+                               self.padding, self.math)
+
+    def replace(self, **kw) -> "Params":
+        d = self.__dict__.copy()
+        d.update(kw)
+        return Params(**d)
+
+
+def _check(st: int, where: str):
+    if st != OK:
+        raise Conv2dError(st, where)
+
+
+def conv2d_output_shape(p: Params):
+    o = (ctypes.c_int32 * 4)()
+    pd = (ctypes.c_int32 * 4)()
+    _check(_lib.conv2d_output_shape(ctypes.byref(p.c()), o, pd), "conv2d_output_shape")
+    return tuple(o), tuple(pd)
+
+
+def conv2d_flop_count(p: Params) -> int:
+    v = ctypes.c_uint64()
+    _check(_lib.conv2d_flop_count(ctypes.byref(p.c()), ctypes.byref(v)), "conv2d_flop_count")
+    return int(v.value)
+
+
+def conv2d_supports(p: Params, algo: int) -> bool:
+    v = ctypes.c_int()
+    _check(_lib.conv2d_supports(ctypes.byref(p.c()), int(algo), ctypes.byref(v)), "conv2d_supports")
+    return bool(v.value)
+
+
+def conv2d_query_workspace(p: Params, algo: int) -> int:
+    v = ctypes.c_size_t()
+    _check(_lib.conv2d_query_workspace(ctypes.byref(p.c()), int(algo), ctypes.byref(v)), "conv2d_query_workspace")
+    return int(v.value)
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return t if isinstance(t, int) else t.data_ptr()
+
+
+def conv2d_forward(p: Params, algo: int, x, w, y, ws=None, ws_bytes: int | None = None, stream=None) -> None:
+    """x, w, y, ws: torch CUDA tensors (or raw device pointers as ints)."""
+    if ws_bytes is None:
+        ws_bytes = 0 if ws is None or isinstance(ws, int) else ws.numel() * ws.element_size()
+    st = _lib.conv2d_forward(ctypes.byref(p.c()), int(algo), _ptr(x), _ptr(w), _ptr(y), _ptr(ws), ws_bytes,
+                             _stream_ptr(stream))
+    _check(st, f"conv2d_forward({conv2d_algo_name(algo)})")
+
+
+def conv2d_autotune(p: Params, x, w, y, ws=None, ws_bytes: int | None = None, stream=None) -> int:
+    if ws_bytes is None:
+        ws_bytes = 0 if ws is None or isinstance(ws, int) else ws.numel() * ws.element_size()
+    a = ctypes.c_int()
+    _check(_lib.conv2d_autotune(ctypes.byref(p.c()), _ptr(x), _ptr(w), _ptr(y), _ptr(ws), ws_bytes,
+                                _stream_ptr(stream), ctypes.byref(a)), "conv2d_autotune")
+    return int(a.value)
+
+
+def conv2d_selected(p: Params):
+    a = ctypes.c_int()
+    st = _lib.conv2d_selected(ctypes.byref(p.c()), ctypes.byref(a))
+    return int(a.value) if st == OK else None
+
+
+def conv2d_set_selected(p: Params, algo: int) -> None:
+    _check(_lib.conv2d_set_selected(ctypes.byref(p.c()), int(algo)), "conv2d_set_selected")
+
+
+def conv2d_clear_selection_cache() -> None:
+    _lib.conv2d_clear_selection_cache()
+
+
+def conv2d_last_tune_times():
+    arr = (ctypes.c_double * NUM_ALGOS)()
+    _lib.conv2d_last_tune_times(arr)
+    return {ALGO_NAMES[i]: arr[i] for i in range(1, NUM_ALGOS) if arr[i] >= 0}
+
+
+def conv2d_launch_count(p: Params, algo: int) -> int:
+    return int(_lib.conv2d_launch_count(ctypes.byref(p.c()), int(algo)))
+
+
+def conv2d_synth_fill(dst, count: int, key: int, offset: int = 0, dist: int = 0, stream=None) -> None:
+    _check(_lib.conv2d_synth_fill(_ptr(dst), count, key, offset, dist, _stream_ptr(stream)), "conv2d_synth_fill")
+
+
+def conv2d_algo_name(a: int) -> str:
+    return _lib.conv2d_algo_name(int(a)).decode()
+
+
+def conv2d_status_string(s: int) -> str:
+    return _lib.conv2d_status_string(int(s)).decode()
+
+
+def conv2d_last_error() -> str:
+    return _lib.conv2d_last_error().decode()
+
+
+# ------------------------------------------------------------------ convenience (torch in, torch out)
+def params_for(x, w, stride=(1, 1), padding: int = PAD_SAME, math: int = MATH_FP32) -> Params:
+    n, h, wd, c = x.shape
+    kh, kw, c2, f = w.shape
+    if c != c2:
+        raise ValueError(f"channel mismatch: input C={c}, filter C={c2}")
+    return Params(n, h, wd, c, f, kh, kw, stride[0], stride[1], padding, math)
+
+
+def forward(x, w, stride=(1, 1), padding: int = PAD_SAME, algo: int = ALGO_AUTO, math: int = MATH_FP32,
+            out=None, workspace=None, stream=None):
+    """y = conv2d(x NHWC fp32 CUDA, w HWCF fp32 CUDA) through conv2d_forward."""
+    import torch
+    p = params_for(x, w, stride, padding, math)
+    (n, ho, wo, f), _ = conv2d_output_shape(p)
+    if not (x.is_cuda and w.is_cuda and x.dtype == torch.float32 and w.dtype == torch.float32):
+        raise ValueError("x and w must be float32 CUDA tensors")
+    x = x.contiguous()
+    w = w.contiguous()
+    y = out if out is not None else torch.empty((n, ho, wo, f), dtype=torch.float32, device=x.device)
+    need = conv2d_query_workspace(p, algo)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device) if need else None
+    conv2d_forward(p, algo, x, w, y, workspace, need if workspace is not None else 0, stream)
+    return y

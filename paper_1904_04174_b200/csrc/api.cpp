@@ -1,0 +1,440 @@
+// api.cpp -- the C-ABI of libconv2d.so (include/conv2d.h): validation, shape inference,
+// workspace sizing, dispatch to the sm_100a kernels, and the measured-time auto-selector.
+//
+// Auto-selection follows the paper's adaptation model -- "the library can adapt to
+// different hardware characteristics by either choosing different algorithms or
+// different parameters for each algorithm", automated as planned in
+// with SPEC.md:333-350's empirical argmin: every supported algorithm
+// is timed with CUDA events (best of R after W warm-ups), ties go to enum order, and the
+// choice is cached per (params, device).
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+
+#include "internal.h"
+
+using namespace conv2d;
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local double g_tune_times[CONV2D_NUM_ALGOS] = {-1, -1, -1, -1, -1, -1};
+
+conv2d_status_t fail(conv2d_status_t s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+conv2d_status_t cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return CONV2D_ERR_CUDA;
+}
+
+bool shape_of(const conv2d_params_t* p, Problem* out, std::string* why) {
+  if (!p) {
+    *why = "params is NULL";
+    return false;
+  }
+  if (p->batch < 1 || p->in_rows < 1 || p->in_cols < 1 || p->channels < 1 || p->features < 1 ||
+      p->window_rows < 1 || p->window_cols < 1 || p->stride_rows < 1 || p->stride_cols < 1) {
+    *why = "every dimension, window and stride must be >= 1";
+    return false;
+  }
+  if (p->math != CONV2D_MATH_FP32 && p->math != CONV2D_MATH_TF32) {
+    *why = "unknown math mode";
+    return false;
+  }
+  Problem q{};
+  q.N = p->batch; q.H = p->in_rows; q.W = p->in_cols; q.C = p->channels; q.F = p->features;
+  q.KH = p->window_rows; q.KW = p->window_cols; q.SH = p->stride_rows; q.SW = p->stride_cols;
+  q.math = p->math;
+  // SPEC.md:48-56 shape algebra (reading R3: SAME pads floor-before / rest-after)
+  if (p->padding == CONV2D_PAD_SAME) {
+    q.HO = (q.H + q.SH - 1) / q.SH;
+    q.WO = (q.W + q.SW - 1) / q.SW;
+    const int64_t tr = std::max<int64_t>((int64_t)(q.HO - 1) * q.SH + q.KH - q.H, 0);
+    const int64_t tc = std::max<int64_t>((int64_t)(q.WO - 1) * q.SW + q.KW - q.W, 0);
+    q.pad_top = (int)(tr / 2);
+    q.pad_left = (int)(tc / 2);
+  } else if (p->padding == CONV2D_PAD_VALID) {
+    if (q.KH > q.H || q.KW > q.W) {
+      *why = "VALID padding requires window <= input extent";
+      return false;
+    }
+    q.HO = (q.H - q.KH) / q.SH + 1;
+    q.WO = (q.W - q.KW) / q.SW + 1;
+    q.pad_top = q.pad_left = 0;
+  } else {
+    *why = "unknown padding mode";
+    return false;
+  }
+  // overflow / index-width guard (reading R20): GEMM rows fit int32 tiles, sizes fit 2^40 elements
+  const int64_t lim = int64_t(1) << 40;
+  if (q.M() > INT_MAX - 256 || q.in_elems() > lim || q.out_elems() > lim || q.filt_elems() > lim ||
+      q.K() > INT_MAX / 2) {
+    *why = "tensor too large (element count overflow guard)";
+    return false;
+  }
+  *out = q;
+  return true;
+}
+
+bool algo_supports(const Problem& q, conv2d_algo_t a) {
+  switch (a) {
+    case CONV2D_ALGO_AUTO:
+    case CONV2D_ALGO_DIRECT:
+    case CONV2D_ALGO_IMPLICIT_GEMM:
+      return true;
+    case CONV2D_ALGO_TILED: {
+      const int CC = q.C < 8 ? q.C : 8;
+      const size_t smem = sizeof(float) * ((size_t)((7) * q.SH + q.KH) * ((15) * q.SW + q.KW) * (CC + 1) +
+                                           (size_t)q.KH * q.KW * CC * 64);
+      return smem <= 227 * 1024;
+    }
+    case CONV2D_ALGO_MATMUL_1X1:
+      return q.KH == 1 && q.KW == 1 && q.SH == 1 && q.SW == 1;
+    case CONV2D_ALGO_WINOGRAD_F2X2_3X3:
+      return q.KH == 3 && q.KW == 3 && q.SH == 1 && q.SW == 1 && q.C >= 32;
+  }
+  return false;
+}
+
+size_t algo_workspace(const Problem& q, conv2d_algo_t a) {
+  switch (a) {
+    case CONV2D_ALGO_IMPLICIT_GEMM: return igemm_workspace(q, false);
+    case CONV2D_ALGO_MATMUL_1X1: return igemm_workspace(q, true);
+    case CONV2D_ALGO_WINOGRAD_F2X2_3X3: return winograd_workspace(q);
+    default: return 0;
+  }
+}
+
+int algo_launches(const Problem& q, conv2d_algo_t a) {
+  switch (a) {
+    case CONV2D_ALGO_DIRECT:
+    case CONV2D_ALGO_TILED: return 1;
+    case CONV2D_ALGO_IMPLICIT_GEMM: return igemm_launches(q, false);
+    case CONV2D_ALGO_MATMUL_1X1: return igemm_launches(q, true);
+    case CONV2D_ALGO_WINOGRAD_F2X2_3X3: return winograd_launches(q);
+    default: return -1;
+  }
+}
+
+// ---- device check (sm_100 only: the kernels are built for sm_100a exclusively)
+std::mutex g_dev_mu;
+std::map<int, bool> g_dev_ok;
+
+conv2d_status_t check_device(int* dev_out) {
+  int dev = -1;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  auto it = g_dev_ok.find(dev);
+  if (it == g_dev_ok.end()) {
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    it = g_dev_ok.emplace(dev, major == 10 && minor == 0).first;
+  }
+  if (!it->second) return fail(CONV2D_ERR_NO_DEVICE, "current device is not sm_100 (B200)");
+  if (dev_out) *dev_out = dev;
+  return CONV2D_OK;
+}
+
+// ---- selector cache: key = all params + device
+using Key = std::tuple<int, int, int, int, int, int, int, int, int, int, int, int>;
+Key key_of(const conv2d_params_t* p, int dev) {
+  return Key(p->batch, p->in_rows, p->in_cols, p->channels, p->features, p->window_rows, p->window_cols,
+             p->stride_rows, p->stride_cols, (int)p->padding, (int)p->math, dev);
+}
+std::mutex g_cache_mu;
+std::map<Key, conv2d_algo_t> g_cache;
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+conv2d_status_t run_algo(const Problem& q, conv2d_algo_t a, const float* in, const float* filt, float* out, void* ws,
+                         cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  switch (a) {
+    case CONV2D_ALGO_DIRECT: e = launch_direct(q, in, filt, out, s); break;
+    case CONV2D_ALGO_TILED: e = launch_tiled(q, in, filt, out, s); break;
+    case CONV2D_ALGO_IMPLICIT_GEMM: e = launch_igemm(q, false, in, filt, out, ws, s); break;
+    case CONV2D_ALGO_MATMUL_1X1: e = launch_igemm(q, true, in, filt, out, ws, s); break;
+    case CONV2D_ALGO_WINOGRAD_F2X2_3X3: e = launch_winograd(q, in, filt, out, ws, s); break;
+    default: return fail(CONV2D_ERR_UNSUPPORTED, "no algorithm to run");
+  }
+  if (e != cudaSuccess) return cuda_fail(e, conv2d_algo_name(a));
+  return CONV2D_OK;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  return atoi(v);
+}
+
+conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int dev, const float* in, const float* filt,
+                              float* out, void* ws, cudaStream_t s, conv2d_algo_t* chosen) {
+  const int warm = std::max(1, env_int("CONV2D_AUTOTUNE_WARMUPS", 2));
+  const int reps = std::max(1, env_int("CONV2D_AUTOTUNE_REPS", 5));
+  for (int i = 0; i < CONV2D_NUM_ALGOS; ++i) g_tune_times[i] = -1.0;
+  cudaEvent_t e0, e1;
+  cudaError_t ce = cudaEventCreate(&e0);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaEventCreate");
+  ce = cudaEventCreate(&e1);
+  if (ce != cudaSuccess) {
+    cudaEventDestroy(e0);
+    return cuda_fail(ce, "cudaEventCreate");
+  }
+  conv2d_algo_t best = CONV2D_ALGO_AUTO;
+  double best_t = 1e300;
+  conv2d_status_t st = CONV2D_OK;
+  for (int ai = 1; ai < CONV2D_NUM_ALGOS && st == CONV2D_OK; ++ai) {
+    const conv2d_algo_t a = (conv2d_algo_t)ai;
+    if (!algo_supports(q, a)) continue;
+    for (int w = 0; w < warm && st == CONV2D_OK; ++w) st = run_algo(q, a, in, filt, out, ws, s);
+    double t_best = 1e300;
+    for (int r = 0; r < reps && st == CONV2D_OK; ++r) {
+      cudaEventRecord(e0, s);
+      st = run_algo(q, a, in, filt, out, ws, s);
+      cudaEventRecord(e1, s);
+      ce = cudaEventSynchronize(e1);
+      if (ce != cudaSuccess) {
+        st = cuda_fail(ce, "autotune sync");
+        break;
+      }
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < t_best) t_best = ms;
+    }
+    if (st != CONV2D_OK) break;
+    g_tune_times[ai] = t_best * 1000.0;
+    if (t_best < best_t) {  // strict: ties keep the earlier enum
+      best_t = t_best;
+      best = a;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (st != CONV2D_OK) return st;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache[key_of(p, dev)] = best;
+  }
+  if (chosen) *chosen = best;
+  return CONV2D_OK;
+}
+
+size_t auto_workspace(const Problem& q) {
+  size_t m = 0;
+  for (int ai = 1; ai < CONV2D_NUM_ALGOS; ++ai)
+    if (algo_supports(q, (conv2d_algo_t)ai)) m = std::max(m, algo_workspace(q, (conv2d_algo_t)ai));
+  return m;
+}
+
+bool valid_algo(conv2d_algo_t a) { return (int)a >= 0 && (int)a < CONV2D_NUM_ALGOS; }
+
+}  // namespace
+
+extern "C" {
+
+conv2d_status_t conv2d_output_shape(const conv2d_params_t* p, int32_t out_nhwf[4], int32_t pads_tblr[4]) {
+  Problem q;
+  std::string why;
+  if (!shape_of(p, &q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
+  if (out_nhwf) {
+    out_nhwf[0] = q.N; out_nhwf[1] = q.HO; out_nhwf[2] = q.WO; out_nhwf[3] = q.F;
+  }
+  if (pads_tblr) {
+    const int tr = std::max((q.HO - 1) * q.SH + q.KH - q.H, 0);
+    const int tc = std::max((q.WO - 1) * q.SW + q.KW - q.W, 0);
+    if (p->padding == CONV2D_PAD_VALID) {
+      pads_tblr[0] = pads_tblr[1] = pads_tblr[2] = pads_tblr[3] = 0;
+    } else {
+      pads_tblr[0] = q.pad_top; pads_tblr[1] = tr - q.pad_top;
+      pads_tblr[2] = q.pad_left; pads_tblr[3] = tc - q.pad_left;
+    }
+  }
+  return CONV2D_OK;
+}
+
+conv2d_status_t conv2d_flop_count(const conv2d_params_t* p, uint64_t* flops) {
+  Problem q;
+  std::string why;
+  if (!flops) return fail(CONV2D_ERR_NULL, "flops is NULL");
+  if (!shape_of(p, &q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
+  *flops = 2ull * (uint64_t)q.M() * (uint64_t)q.K() * (uint64_t)q.F;
+  return CONV2D_OK;
+}
+
+conv2d_status_t conv2d_supports(const conv2d_params_t* p, conv2d_algo_t algo, int* supported) {
+  Problem q;
+  std::string why;
+  if (!supported) return fail(CONV2D_ERR_NULL, "supported is NULL");
+  if (!shape_of(p, &q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
+  if (!valid_algo(algo)) return fail(CONV2D_ERR_INVALID_PARAMS, "unknown algorithm");
+  *supported = algo_supports(q, algo) ? 1 : 0;
+  return CONV2D_OK;
+}
+
+conv2d_status_t conv2d_query_workspace(const conv2d_params_t* p, conv2d_algo_t algo, size_t* bytes) {
+  Problem q;
+  std::string why;
+  if (!bytes) return fail(CONV2D_ERR_NULL, "bytes is NULL");
+  if (!shape_of(p, &q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
+  if (!valid_algo(algo)) return fail(CONV2D_ERR_INVALID_PARAMS, "unknown algorithm");
+  if (!algo_supports(q, algo)) return fail(CONV2D_ERR_UNSUPPORTED, "algorithm does not support these params");
+  *bytes = algo == CONV2D_ALGO_AUTO ? auto_workspace(q) : algo_workspace(q, algo);
+  return CONV2D_OK;
+}
+
+static conv2d_status_t validate_call(const conv2d_params_t* p, conv2d_algo_t algo, const float* in, const float* filt,
+                                     float* out, void* ws, size_t ws_bytes, Problem* q) {
+  std::string why;
+  if (!shape_of(p, q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
+  if (!valid_algo(algo)) return fail(CONV2D_ERR_INVALID_PARAMS, "unknown algorithm");
+  if (!algo_supports(*q, algo))
+    return fail(CONV2D_ERR_UNSUPPORTED, std::string(conv2d_algo_name(algo)) + " does not support these params");
+  if (!in || !filt || !out) return fail(CONV2D_ERR_NULL, "in/filt/out must be non-NULL device pointers");
+  if (!aligned16(in) || !aligned16(filt) || !aligned16(out) || (ws && !aligned16(ws)))
+    return fail(CONV2D_ERR_ALIGNMENT, "device pointers must be 16-byte aligned");
+  const size_t need = algo == CONV2D_ALGO_AUTO ? auto_workspace(*q) : algo_workspace(*q, algo);
+  if (need > 0 && (!ws || ws_bytes < need))
+    return fail(CONV2D_ERR_WORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
+  return CONV2D_OK;
+}
+
+conv2d_status_t conv2d_forward(const conv2d_params_t* p, conv2d_algo_t algo, const float* in, const float* filt,
+                               float* out, void* ws, size_t ws_bytes, void* stream) {
+  Problem q;
+  conv2d_status_t st = validate_call(p, algo, in, filt, out, ws, ws_bytes, &q);
+  if (st != CONV2D_OK) return st;
+  int dev = -1;
+  st = check_device(&dev);
+  if (st != CONV2D_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  conv2d_algo_t a = algo;
+  if (a == CONV2D_ALGO_AUTO) {
+    bool hit = false;
+    {
+      std::lock_guard<std::mutex> lk(g_cache_mu);
+      auto it = g_cache.find(key_of(p, dev));
+      if (it != g_cache.end()) {
+        a = it->second;
+        hit = true;
+      }
+    }
+    if (!hit) {
+      st = autotune_impl(p, q, dev, in, filt, out, ws, s, &a);
+      if (st != CONV2D_OK) return st;
+    }
+  }
+  return run_algo(q, a, in, filt, out, ws, s);
+}
+
+conv2d_status_t conv2d_autotune(const conv2d_params_t* p, const float* in, const float* filt, float* out, void* ws,
+                                size_t ws_bytes, void* stream, conv2d_algo_t* chosen) {
+  Problem q;
+  conv2d_status_t st = validate_call(p, CONV2D_ALGO_AUTO, in, filt, out, ws, ws_bytes, &q);
+  if (st != CONV2D_OK) return st;
+  int dev = -1;
+  st = check_device(&dev);
+  if (st != CONV2D_OK) return st;
+  return autotune_impl(p, q, dev, in, filt, out, ws, static_cast<cudaStream_t>(stream), chosen);
+}
+
+conv2d_status_t conv2d_selected(const conv2d_params_t* p, conv2d_algo_t* chosen) {
+  Problem q;
+  std::string why;
+  if (!chosen) return fail(CONV2D_ERR_NULL, "chosen is NULL");
+  *chosen = CONV2D_ALGO_AUTO;
+  if (!shape_of(p, &q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = g_cache.find(key_of(p, dev));
+  if (it == g_cache.end()) return fail(CONV2D_ERR_UNSUPPORTED, "not cached");
+  *chosen = it->second;
+  return CONV2D_OK;
+}
+
+conv2d_status_t conv2d_set_selected(const conv2d_params_t* p, conv2d_algo_t algo) {
+  Problem q;
+  std::string why;
+  if (!shape_of(p, &q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
+  if (!valid_algo(algo) || algo == CONV2D_ALGO_AUTO) return fail(CONV2D_ERR_INVALID_PARAMS, "need a concrete algorithm");
+  if (!algo_supports(q, algo)) return fail(CONV2D_ERR_UNSUPPORTED, "algorithm does not support these params");
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache[key_of(p, dev)] = algo;
+  return CONV2D_OK;
+}
+
+void conv2d_clear_selection_cache(void) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache.clear();
+}
+
+void conv2d_last_tune_times(double times_us[CONV2D_NUM_ALGOS]) {
+  if (!times_us) return;
+  for (int i = 0; i < CONV2D_NUM_ALGOS; ++i) times_us[i] = g_tune_times[i];
+}
+
+int conv2d_launch_count(const conv2d_params_t* p, conv2d_algo_t algo) {
+  Problem q;
+  std::string why;
+  if (!shape_of(p, &q, &why) || !valid_algo(algo)) return -1;
+  if (algo == CONV2D_ALGO_AUTO) {
+    conv2d_algo_t a;
+    if (conv2d_selected(p, &a) != CONV2D_OK) return -1;
+    algo = a;
+  }
+  if (!algo_supports(q, algo)) return -1;
+  return algo_launches(q, algo);
+}
+
+conv2d_status_t conv2d_synth_fill(float* dst, uint64_t count, uint64_t key, uint64_t offset, int dist, void* stream) {
+  if (!dst && count) return fail(CONV2D_ERR_NULL, "dst is NULL");
+  if (dist != 0 && dist != 1) return fail(CONV2D_ERR_INVALID_PARAMS, "dist must be 0 or 1");
+  conv2d_status_t st = check_device(nullptr);
+  if (st != CONV2D_OK) return st;
+  cudaError_t e = launch_synth_fill(dst, count, key, offset, dist, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "synth_fill");
+  return CONV2D_OK;
+}
+
+const char* conv2d_status_string(conv2d_status_t s) {
+  switch (s) {
+    case CONV2D_OK: return "CONV2D_OK";
+    case CONV2D_ERR_INVALID_PARAMS: return "CONV2D_ERR_INVALID_PARAMS";
+    case CONV2D_ERR_UNSUPPORTED: return "CONV2D_ERR_UNSUPPORTED";
+    case CONV2D_ERR_WORKSPACE: return "CONV2D_ERR_WORKSPACE";
+    case CONV2D_ERR_ALIGNMENT: return "CONV2D_ERR_ALIGNMENT";
+    case CONV2D_ERR_NULL: return "CONV2D_ERR_NULL";
+    case CONV2D_ERR_CUDA: return "CONV2D_ERR_CUDA";
+    case CONV2D_ERR_NO_DEVICE: return "CONV2D_ERR_NO_DEVICE";
+  }
+  return "CONV2D_ERR_UNKNOWN";
+}
+
+const char* conv2d_algo_name(conv2d_algo_t a) {
+  switch (a) {
+    case CONV2D_ALGO_AUTO: return "auto";
+    case CONV2D_ALGO_DIRECT: return "direct";
+    case CONV2D_ALGO_TILED: return "tiled";
+    case CONV2D_ALGO_IMPLICIT_GEMM: return "implicit_gemm";
+    case CONV2D_ALGO_WINOGRAD_F2X2_3X3: return "winograd_f2x2_3x3";
+    case CONV2D_ALGO_MATMUL_1X1: return "matmul_1x1";
+  }
+  return "unknown";
+}
+
+const char* conv2d_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

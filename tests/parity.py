@@ -1,0 +1,73 @@
+"""Shared parity helpers for the GPU tests (test infrastructure; imports the oracle).
+
+CUDA side: paper_1904_04174_b200.conv2d (the C-ABI binding).  Oracle side: oracle/.
+Inputs for both come from paper_1904_04174_b200.synth only.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle as O
+from paper_1904_04174_b200 import synth
+
+TOL_FP32 = 1e-5   # north_star: fp32 and 3xTF32
+TOL_TF32 = 2e-3   # north_star: plain TF32
+
+_C = None
+
+
+def C():
+    global _C
+    if _C is None:
+        from paper_1904_04174_b200 import build
+        build.build()
+        from paper_1904_04174_b200 import conv2d
+        _C = conv2d
+    return _C
+
+
+def tol_for(algo: int, math: int) -> float:
+    c = C()
+    if math == c.MATH_TF32 and algo in (c.ALGO_IMPLICIT_GEMM, c.ALGO_MATMUL_1X1, c.ALGO_WINOGRAD_F2X2_3X3,
+                                        c.ALGO_AUTO):
+        return TOL_TF32
+    return TOL_FP32
+
+
+def oparams(p) -> O.Params:
+    return O.Params(p.batch, p.in_rows, p.in_cols, p.channels, p.features, p.window_rows, p.window_cols,
+                    p.stride_rows, p.stride_cols, p.padding)
+
+
+def make_inputs(p, layer_id: int = 0, dist: int = synth.DIST_UNIFORM):
+    x = synth.input_nhwc(p.batch, p.in_rows, p.in_cols, p.channels, layer_id=layer_id, dist=dist)
+    w = synth.filter_hwcf(p.window_rows, p.window_cols, p.channels, p.features, layer_id=layer_id, dist=dist)
+    return x, w
+
+
+def gpu_conv(p, x: np.ndarray, w: np.ndarray, algo: int) -> np.ndarray:
+    import torch
+    c = C()
+    xd = torch.from_numpy(x).cuda()
+    wd = torch.from_numpy(w).cuda()
+    (n, ho, wo, f), _ = c.conv2d_output_shape(p)
+    y = torch.full((n, ho, wo, f), float("nan"), dtype=torch.float32, device="cuda")  # poison: catches unwritten outputs
+    need = c.conv2d_query_workspace(p, algo)
+    ws = torch.full((max(need, 16),), 0xFF, dtype=torch.uint8, device="cuda") if need else None
+    c.conv2d_forward(p, algo, xd, wd, y, ws, need)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def supported_algos(p):
+    c = C()
+    return [a for a in range(1, c.NUM_ALGOS) if c.conv2d_supports(p, a)]
+
+
+def check_close(p, y: np.ndarray, y_ref: np.ndarray, denom: np.ndarray, algo: int, what: str = ""):
+    assert y.shape == y_ref.shape, (what, y.shape, y_ref.shape)
+    assert np.all(np.isfinite(y)), f"{what}: non-finite output (unwritten or NaN)"
+    e = O.normalized_error(y, y_ref, denom)
+    tol = tol_for(algo, p.math)
+    assert e <= tol, f"{what}: normalized error {e:.3e} > {tol:.0e}"
+    return e

@@ -1,0 +1,195 @@
+"""GPU parity: every algorithm x math mode of libconv2d.so (called through the C-ABI)
+against the CPU oracle on the same seeded inputs (north_star tolerance:
+max|err| / sum|x||w| <= 1e-5 for fp32 and 3xTF32, <= 2e-3 for TF32; shapes bit-exact).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1904_04174_b200 import layers as L
+from paper_1904_04174_b200 import synth
+
+from .parity import C, check_close, gpu_conv, make_inputs, oparams, supported_algos
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+MATHS = (0, 1)  # FP32 (3xTF32 on tensor paths), TF32
+
+
+def P(batch, h, w, c, f, kh, kw, sh=1, sw=1, pad=0, math=0):
+    return C().Params(batch, h, w, c, f, kh, kw, sh, sw, pad, math)
+
+
+def test_config1_golden_integer_all_algos(cuda_ok):
+    g = json.load(open(os.path.join(GOLD, "config1_integer.json")))
+    x = np.array([[[[((h * 8 + w) * 4 + c) % 7 - 3 for c in range(4)] for w in range(8)] for h in range(8)]],
+                 dtype=np.float32)
+    wt = np.array([[[[(((kh * 3 + kw) * 4 + c) * 8 + f) % 5 - 2 for f in range(8)] for c in range(4)]
+                    for kw in range(3)] for kh in range(3)], dtype=np.float32)
+    for key in ("same_s1", "valid_s1", "same_s2"):
+        e = g[key]
+        for math in MATHS:
+            p = P(1, 8, 8, 4, 8, 3, 3, e["stride"], e["stride"], 0 if e["padding"] == "SAME" else 1, math)
+            ref = O.conv2d(oparams(p), x, wt)
+            for a in supported_algos(p):
+                y = gpu_conv(p, x, wt, a)
+                assert list(y.shape) == e["shape"]
+                assert np.array_equal(y, ref), (key, math, C().conv2d_algo_name(a))
+                for (n, i, j, f, v) in e["points"]:
+                    assert y[n, i, j, f] == v
+                assert y.sum() == e["sum"]
+
+
+ALL_SHAPES = [l for l in L.RESNET50_SETS] + [l for l, _ in L.VGG16_LAYERS]
+
+
+@pytest.mark.parametrize("layer", ALL_SHAPES, ids=lambda l: l.name)
+def test_exact_integer_regime_b1(cuda_ok, layer):
+    """P7: integer data in [-2,2] makes every partial sum exact -> every algorithm bit-exact."""
+    p0 = P(**layer.params(1))
+    x, w = make_inputs(p0, layer_id=100, dist=synth.DIST_INT5)
+    ref = O.conv2d(oparams(p0), x, w)
+    for math in MATHS:
+        p = p0.replace(math=math)
+        for a in supported_algos(p):
+            y = gpu_conv(p, x, w, a)
+            assert np.array_equal(y, ref), (layer.name, math, C().conv2d_algo_name(a),
+                                            int(np.sum(y != ref)))
+
+
+@pytest.mark.parametrize("layer", ALL_SHAPES, ids=lambda l: l.name)
+def test_uniform_paper_shapes_b1(cuda_ok, layer):
+    p0 = P(**layer.params(1))
+    x, w = make_inputs(p0, layer_id=200)
+    ref, den = O.conv2d(oparams(p0), x, w, with_denom=True)
+    for math in MATHS:
+        p = p0.replace(math=math)
+        for a in supported_algos(p):
+            check_close(p, gpu_conv(p, x, w, a), ref, den, a, f"{layer.name} math={math} {C().conv2d_algo_name(a)}")
+
+
+def _fuzz_cases(n=200, seed=1234):
+    # SPEC.md:278 / 534: spatial 1..20, C,F 1..32, K in {1,3,5,7}, S in {1,2}, both paddings, batch 1..3
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        k = int(rng.choice([1, 3, 5, 7]))
+        h, w = int(rng.integers(1, 21)), int(rng.integers(1, 21))
+        pad = int(rng.integers(0, 2))
+        if pad == 1 and (k > h or k > w):
+            continue
+        out.append((int(rng.integers(1, 4)), h, w, int(rng.integers(1, 33)), int(rng.integers(1, 33)), k, k,
+                    int(rng.integers(1, 3)), int(rng.integers(1, 3)), pad))
+    return out
+
+
+def test_spec_fuzz_200(cuda_ok):
+    for i, case in enumerate(_fuzz_cases()):
+        p0 = P(*case)
+        x, w = make_inputs(p0, layer_id=300 + i)
+        ref, den = O.conv2d(oparams(p0), x, w, with_denom=True)
+        for math in MATHS:
+            p = p0.replace(math=math)
+            for a in supported_algos(p):
+                check_close(p, gpu_conv(p, x, w, a), ref, den, a, f"fuzz {case} math={math} {C().conv2d_algo_name(a)}")
+
+
+EDGE = [
+    (1, 1, 1, 1, 1, 1, 1, 1, 1, 0),          # single element
+    (1, 1, 1, 7, 5, 3, 3, 1, 1, 0),          # window larger than image, SAME
+    (2, 3, 2, 3, 9, 7, 7, 2, 2, 0),          # 7x7 s2 on tiny input
+    (1, 9, 7, 40, 33, 3, 3, 1, 1, 0),        # odd Ho/Wo Winograd tiles, F%4 != 0
+    (3, 15, 9, 64, 70, 3, 3, 1, 1, 1),       # VALID Winograd, ragged N
+    (1, 33, 35, 1, 1, 5, 5, 1, 1, 0),        # C=1, F=1
+    (1, 13, 11, 5, 130, 3, 3, 2, 1, 0),      # C%4 != 0 scalar gather, ragged N tile
+    (2, 7, 7, 2048, 64, 1, 1, 1, 1, 0),      # deep K, split-K
+    (1, 7, 7, 512, 512, 3, 3, 1, 1, 0),      # R24 b1: split-K winograd + igemm
+    (64, 2, 2, 32, 16, 1, 1, 1, 1, 0),       # many images, tiny spatial
+    (1, 20, 20, 96, 257, 1, 1, 1, 1, 0),     # F = 257 (one past a tile)
+    (2, 17, 19, 36, 24, 2, 4, 3, 2, 0),      # non-square window / stride
+    (1, 130, 3, 8, 8, 3, 3, 1, 1, 0),        # M just over one 128-row tile per image row sweep
+]
+
+
+@pytest.mark.parametrize("case", EDGE, ids=str)
+def test_edge_cases(cuda_ok, case):
+    p0 = P(*case)
+    x, w = make_inputs(p0, layer_id=400)
+    ref, den = O.conv2d(oparams(p0), x, w, with_denom=True)
+    xi, wi = make_inputs(p0, layer_id=401, dist=synth.DIST_INT5)
+    refi = O.conv2d(oparams(p0), xi, wi)
+    for math in MATHS:
+        p = p0.replace(math=math)
+        for a in supported_algos(p):
+            check_close(p, gpu_conv(p, x, w, a), ref, den, a, f"edge {case} math={math} {C().conv2d_algo_name(a)}")
+            assert np.array_equal(gpu_conv(p, xi, wi, a), refi), (case, math, a)
+
+
+def test_determinism_and_shard_bitwise(cuda_ok):
+    """P11: fixed (params, algo) -> bitwise identical reruns; batch slices run separately give
+    the same bits as the full batch when the launch configuration is the same."""
+    p = P(4, 28, 28, 64, 64, 3, 3)
+    x, w = make_inputs(p, layer_id=500)
+    for a in supported_algos(p):
+        y1 = gpu_conv(p, x, w, a)
+        y2 = gpu_conv(p, x, w, a)
+        assert np.array_equal(y1, y2), C().conv2d_algo_name(a)
+    ph = p.replace(batch=2)
+    for a in (C().ALGO_DIRECT, C().ALGO_TILED):
+        full = gpu_conv(p, x, w, a)
+        for r in range(2):
+            assert np.array_equal(gpu_conv(ph, x[2 * r:2 * r + 2], w, a), full[2 * r:2 * r + 2])
+
+
+def test_autotune_and_auto_forward(cuda_ok):
+    import torch
+    c = C()
+    c.conv2d_clear_selection_cache()
+    p = P(2, 28, 28, 128, 128, 3, 3)
+    x, w = make_inputs(p, layer_id=600)
+    ref, den = O.conv2d(oparams(p), x, w, with_denom=True)
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    y = torch.empty((2, 28, 28, 128), device="cuda")
+    need = c.conv2d_query_workspace(p, c.ALGO_AUTO)
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    a = c.conv2d_autotune(p, xd, wd, y, ws, need)
+    assert a != c.ALGO_AUTO and c.conv2d_supports(p, a)
+    times = c.conv2d_last_tune_times()
+    assert set(times) == {c.ALGO_NAMES[i] for i in supported_algos(p)}
+    assert min(times, key=lambda k: (times[k], c.ALGO_BY_NAME[k])) == c.ALGO_NAMES[a]  # argmin, ties by enum
+    assert c.conv2d_selected(p) == a
+    y.fill_(float("nan"))
+    c.conv2d_forward(p, c.ALGO_AUTO, xd, wd, y, ws, need)
+    torch.cuda.synchronize()
+    check_close(p, y.cpu().numpy(), ref, den, c.ALGO_AUTO, "auto")
+    # AUTO on a cache miss tunes implicitly
+    p2 = p.replace(math=1)
+    assert c.conv2d_selected(p2) is None
+    out = c.forward(xd, wd, algo=c.ALGO_AUTO, math=1)
+    check_close(p2, out.cpu().numpy(), ref, den, c.ALGO_AUTO, "auto tf32")
+    assert c.conv2d_selected(p2) is not None
+
+
+def test_device_synth_matches_host_generator(cuda_ok):
+    import torch
+    c = C()
+    for dist in (0, 1):
+        key = synth.stream_key(synth.SEED, 7, 0)
+        d = torch.empty(100003, device="cuda")
+        c.conv2d_synth_fill(d, d.numel(), key, 12345, dist)
+        torch.cuda.synchronize()
+        assert np.array_equal(d.cpu().numpy(), synth.draw(100003, key, 12345, dist))
+
+
+def test_fault_injection_is_detected(cuda_ok):
+    """P12: a single output perturbed by 1e-2 must fail the parity check."""
+    p = P(1, 14, 14, 32, 32, 3, 3)
+    x, w = make_inputs(p, layer_id=700)
+    ref, den = O.conv2d(oparams(p), x, w, with_denom=True)
+    y = gpu_conv(p, x, w, C().ALGO_IMPLICIT_GEMM)
+    y[0, 5, 5, 5] += 1e-2
+    with pytest.raises(AssertionError):
+        check_close(p, y, ref, den, C().ALGO_IMPLICIT_GEMM, "fault")
