@@ -93,8 +93,8 @@ bool algo_supports(const Problem& q, conv2d_algo_t a) {
       return true;
     case CONV2D_ALGO_TILED: {
       const int CC = q.C < 8 ? q.C : 8;
-      const size_t smem = sizeof(float) * ((size_t)((7) * q.SH + q.KH) * ((15) * q.SW + q.KW) * (CC + 1) +
-                                           (size_t)q.KH * q.KW * CC * 64);
+      const size_t xs = (size_t)(7 * q.SH + q.KH) * (15 * q.SW + q.KW) * (CC + 1);
+      const size_t smem = sizeof(float) * ((xs + 3) / 4 * 4 + (size_t)q.KH * q.KW * CC * 64);
       return smem <= 227 * 1024;
     }
     case CONV2D_ALGO_MATMUL_1X1:

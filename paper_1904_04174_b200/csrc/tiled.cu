@@ -28,8 +28,8 @@ __global__ void __launch_bounds__(NTHREADS) tiled_kernel(const float* __restrict
   const int CCP = CC + 1;
   const int IH = (TH - 1) * SH + KH;
   const int IW = (TW - 1) * SW + KW;
-  float* xs = smem;                      // [IH][IW][CCP]
-  float* ws = smem + IH * IW * CCP;      // [KH][KW][CC][FB]
+  float* xs = smem;                                  // [IH][IW][CCP]
+  float* ws = smem + ((IH * IW * CCP + 3) & ~3);     // [KH][KW][CC][FB], 16-byte aligned for LDS.128
 
   const int n = blockIdx.z / fblocks;
   const int fb0 = (blockIdx.z % fblocks) * FB;
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(NTHREADS) tiled_kernel(const float* __restrict
 cudaError_t launch_tiled(const Problem& p, const float* in, const float* filt, float* out, cudaStream_t s) {
   const int CC = p.C < CCMAX ? p.C : CCMAX;
   const int IH = (TH - 1) * p.SH + p.KH, IW = (TW - 1) * p.SW + p.KW;
-  const size_t smem = sizeof(float) * ((size_t)IH * IW * (CC + 1) + (size_t)p.KH * p.KW * CC * FB);
+  const size_t smem = sizeof(float) * ((((size_t)IH * IW * (CC + 1)) + 3) / 4 * 4 + (size_t)p.KH * p.KW * CC * FB);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   static bool attr_set = false;  // benign race: idempotent
   if (!attr_set) {

@@ -49,7 +49,7 @@ ALL_SHAPES = [l for l in L.RESNET50_SETS] + [l for l, _ in L.VGG16_LAYERS]
 @pytest.mark.parametrize("layer", ALL_SHAPES, ids=lambda l: l.name)
 def test_exact_integer_regime_b1(cuda_ok, layer):
     """P7: integer data in [-2,2] makes every partial sum exact -> every algorithm bit-exact."""
-    p0 = P(**layer.params(1))
+    p0 = C().Params(**layer.params(1))
     x, w = make_inputs(p0, layer_id=100, dist=synth.DIST_INT5)
     ref = O.conv2d(oparams(p0), x, w)
     for math in MATHS:
@@ -62,7 +62,7 @@ def test_exact_integer_regime_b1(cuda_ok, layer):
 
 @pytest.mark.parametrize("layer", ALL_SHAPES, ids=lambda l: l.name)
 def test_uniform_paper_shapes_b1(cuda_ok, layer):
-    p0 = P(**layer.params(1))
+    p0 = C().Params(**layer.params(1))
     x, w = make_inputs(p0, layer_id=200)
     ref, den = O.conv2d(oparams(p0), x, w, with_denom=True)
     for math in MATHS:
