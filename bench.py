@@ -1,0 +1,455 @@
+#!/usr/bin/env python
+"""bench.py -- conv2d forward GFLOP/s on B200 (BASELINE.json metric), 1..8 GPUs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--math fp32|tf32] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step = one pass of the ResNet-50 v1.5 conv stack (53 convs, BASELINE.json configs[4],
+DESIGN.md reading R11) over the global batch of 256 images, batch-sharded over the N ranks
+(rank r owns images [r*256/N, (r+1)*256/N); no collective on the data path; strong scaling).
+Every conv has its own seeded synthetic input and filter (device twin of synth.py) and
+runs through conv2d_forward(AUTO): the auto-selector's measured choice per layer.
+
+Rank 0 prints ONE JSON line.  value = total flops of all ranks / max-over-ranks device time.
+Timing: W untimed warm-up steps, then K steps each bracketed by CUDA events on the
+launching stream, L2 flushed (256 MiB write) before every step outside the events, a
+barrier + synchronize on both sides of the timed region; nvidia-smi clocks sampled during
+it.  Also reported: roofline of the dominant kernel group, the CPU oracle baseline, the
+end-to-end number through the public API with pinned host buffers, launch count.
+
+--impl reference times the CPU oracle (oracle/, the only reference this paper-only run
+has) on a bounded sample of the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1904_04174_b200 import layers as L  # noqa: E402
+from paper_1904_04174_b200 import synth  # noqa: E402
+
+METRIC = "conv2d forward GFLOP/s per VGG/ResNet layer, % of B200 peak, 1/2/4/8 GPUs"
+GLOBAL_BATCH = 256
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def layer_bytes(l, batch):
+    """Algorithmic bytes: touched input + filter + output, fp32."""
+    ho = -(-l.rows // l.stride)
+    wo = -(-l.cols // l.stride)
+    if l.window == 1 and l.stride > 1:
+        touched = batch * ho * wo * l.channels  # strided 1x1 reads only the sampled pixels
+    else:
+        touched = batch * l.rows * l.cols * l.channels
+    return 4 * (touched + l.window * l.window * l.channels * l.features + batch * ho * wo * l.features)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons, pw = [], [], set(), []
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                pw.append(float(f[3]))
+            except ValueError:
+                continue
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(pw) if pw else None}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) legs
+def oracle_sample(images: int, math_layers=None):
+    """Host inputs for `images` images of every conv of the stack (global images 0..images-1)."""
+    import oracle as O
+    work = []
+    for conv_id, l in L.resnet50_v15_stack():
+        x = synth.input_nhwc(images, l.rows, l.cols, l.channels, layer_id=conv_id)
+        w = synth.filter_hwcf(l.window, l.window, l.channels, l.features, layer_id=conv_id)
+        op = O.Params(images, l.rows, l.cols, l.channels, l.features, l.window, l.window, l.stride, l.stride, O.SAME)
+        work.append((op, x, w, l.flops(images)))
+    return work
+
+
+def run_oracle(work, threads):
+    import oracle as O
+    t0 = time.perf_counter()
+    for op, x, w, _ in work:
+        O.conv2d(op, x, w, threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(target_s: float = 12.0):
+    """The oracle as it stands, on this host's cores, over a bounded sample of the workload."""
+    import oracle as O
+    O.build()
+    threads = os.cpu_count() or 1
+    w1 = oracle_sample(1)
+    t1 = run_oracle(w1, threads)
+    flops1 = sum(f for *_, f in w1)
+    images = max(1, min(16, int(target_s / max(t1, 1e-3))))
+    if images > 1:
+        wk = oracle_sample(images)
+        t = run_oracle(wk, threads)
+        flops = sum(f for *_, f in wk)
+    else:
+        t, flops = t1, flops1
+    return {"value": round(flops / t / 1e9, 3), "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+            "sample": f"all 53 convs of the ResNet-50 v1.5 stack on {images} image(s) (global images 0..{images-1}),"
+                      f" full oracle incl. double accumulation; {flops/1e9:.2f} GFLOP in {t:.2f} s"}
+
+
+def reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import oracle as O
+    O.build()
+    threads = os.cpu_count() or 1
+    work = oracle_sample(1)
+    flops = sum(f for *_, f in work)
+    for _ in range(args.warmup):
+        run_oracle(work, threads)
+    times = [run_oracle(work, threads) for _ in range(args.steps)]
+    total = sum(times)
+    value = flops * args.steps / total / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * total / args.steps, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64-accumulate",
+            "data": "synthetic", "config": workload_config(args, 1),
+            "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+                             "sample": "each step: all 53 convs of the stack on 1 image (global image 0)"},
+            "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, per_gpu):
+    return {"workload": "resnet50_v1.5_conv_stack (53 convs, BASELINE configs[4])", "global_batch": GLOBAL_BATCH,
+            "per_gpu_batch": per_gpu, "math": "3xtf32 (fp32-faithful)" if args.math == "fp32" else "tf32",
+            "algo": "auto (measured per layer)", "parallelism": f"batch-shard x{args.gpus}",
+            "l2": "flushed before every step (256 MiB write, outside the timed events); step working set ~22 GB",
+            "gflop_per_step": round(sum(l.flops(GLOBAL_BATCH) for _, l in L.resnet50_v15_stack()) / 1e9, 3)}
+
+
+# ----------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--math", choices=["fp32", "tf32"], default="fp32")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layers-out", default="", help="write the per-layer table (JSON) here")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1904_04174_b200 import conv2d as C
+
+    rank, world, local = env_rank()
+    if world != args.gpus:
+        args.gpus = world if world > 1 else args.gpus
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    assert GLOBAL_BATCH % max(world, 1) == 0
+    B = GLOBAL_BATCH // world
+    math = C.MATH_FP32 if args.math == "fp32" else C.MATH_TF32
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- resident inputs (device generator, global image offsets -> shards are exact slices)
+    stack = L.resnet50_v15_stack()
+    convs = []
+    ws_bytes = 0
+    for conv_id, l in stack:
+        p = C.Params(**l.params(B), math=math)
+        (n, ho, wo, f), _ = C.conv2d_output_shape(p)
+        per_img = l.rows * l.cols * l.channels
+        x = torch.empty(B * per_img, dtype=torch.float32, device=dev)
+        C.conv2d_synth_fill(x, x.numel(), synth.stream_key(synth.SEED, conv_id, synth.ROLE_INPUT),
+                            rank * B * per_img, 0)
+        w = torch.empty(l.window * l.window * l.channels * l.features, dtype=torch.float32, device=dev)
+        C.conv2d_synth_fill(w, w.numel(), synth.stream_key(synth.SEED, conv_id, synth.ROLE_FILTER), 0, 0)
+        y = torch.empty(n * ho * wo * f, dtype=torch.float32, device=dev)
+        ws_bytes = max(ws_bytes, C.conv2d_query_workspace(p, C.ALGO_AUTO))
+        convs.append(dict(id=conv_id, layer=l, p=p, x=x, w=w, y=y, flops=C.conv2d_flop_count(p),
+                          bytes=layer_bytes(l, B)))
+    ws = torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    # ---- auto-selection (measured, once per distinct layer); rank 0's choices broadcast so every
+    #      rank runs the same kernels (off the timed path)
+    chosen = {}
+    for cv in convs:
+        key = cv["layer"].name
+        if key not in chosen:
+            chosen[key] = C.conv2d_autotune(cv["p"], cv["x"], cv["w"], cv["y"], ws, ws.numel())
+    if world > 1:
+        names = sorted(chosen)
+        t = torch.tensor([chosen[k] for k in names], dtype=torch.int32, device=dev)
+        dist.broadcast(t, 0)
+        for k, a in zip(names, t.tolist()):
+            chosen[k] = a
+    for cv in convs:
+        C.conv2d_set_selected(cv["p"], chosen[cv["layer"].name])
+        cv["algo"] = chosen[cv["layer"].name]
+        cv["launches"] = C.conv2d_launch_count(cv["p"], C.ALGO_AUTO)
+
+    def step(evs=None):
+        for i, cv in enumerate(convs):
+            if evs is not None:
+                evs[i][0].record(stream)
+            C.conv2d_forward(cv["p"], C.ALGO_AUTO, cv["x"], cv["w"], cv["y"], ws, ws.numel(), stream)
+            if evs is not None:
+                evs[i][1].record(stream)
+
+    for _ in range(max(args.warmup, 1)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region
+    ev_step = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev_conv = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in convs]
+               for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    if rank == 0:
+        clocks.start()
+        time.sleep(0.3)
+    wall0 = time.perf_counter()
+    for k in range(args.steps):
+        flush.zero_()
+        ev_step[k][0].record(stream)
+        step(ev_conv[k])
+        ev_step[k][1].record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    barrier()
+    clk = clocks.stop() if rank == 0 else None
+    t_ms = sum(a.elapsed_time(b) for a, b in ev_step)
+    tmax = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    t_ms = float(tmax.item())
+    flops_step_all = sum(cv["flops"] for cv in convs) * world
+    value = flops_step_all * args.steps / (t_ms / 1e3) / 1e9
+
+    # ---- per-conv times (mean over timed steps) -> per-layer table and dominant kernel group
+    per_conv_ms = [statistics.mean(ev_conv[k][i][0].elapsed_time(ev_conv[k][i][1]) for k in range(args.steps))
+                   for i in range(len(convs))]
+    peaks, peak_src = load_peaks()
+    tf32_peak = peaks["bf16_tflops"] / 2.0             # nominal TF32 : BF16 = 1 : 2 (B200_PROFILING.md)
+    useful_peak = tf32_peak / 3.0 if math == C.MATH_FP32 else tf32_peak  # 3 MMAs per product in 3xTF32
+    hbm = peaks["hbm_gbs"]
+    groups = {}
+    for cv, ms in zip(convs, per_conv_ms):
+        g = groups.setdefault(cv["algo"], {"ms": 0.0, "flops": 0, "bytes": 0, "n": 0})
+        g["ms"] += ms
+        g["flops"] += cv["flops"]
+        g["bytes"] += cv["bytes"]
+        g["n"] += 1
+    dom = max(groups, key=lambda a: groups[a]["ms"])
+    gd = groups[dom]
+    if dom in (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1, C.ALGO_WINOGRAD_F2X2_3X3):
+        ach = gd["flops"] / (gd["ms"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(useful_peak, 1), "unit": "TFLOP/s",
+                "frac": round(ach / useful_peak, 4), "traffic": None,
+                "kernel": f"conv2d_forward[{C.ALGO_NAMES[dom]}] (filter prep + tcgen05 GEMM + split reduce), "
+                          f"{gd['n']} of {len(convs)} convs, {100 * gd['ms'] / sum(per_conv_ms):.1f}% of step",
+                "peak_source": f"{peak_src} bf16 burst {peaks['bf16_tflops']} TF/s /2 (TF32)"
+                               + (" /3 (3xTF32 useful)" if math == C.MATH_FP32 else "")}
+    else:
+        ach = gd["flops"] / (gd["ms"] / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": round(ach, 2), "peak": round(148 * 128 * 2 * 1.965e9 / 1e12, 1),
+                "unit": "TFLOP/s", "frac": round(ach / (148 * 128 * 2 * 1.965e-3), 4), "traffic": None,
+                "kernel": f"conv2d_forward[{C.ALGO_NAMES[dom]}]", "peak_source": "148 SM x 128 FFMA x 2 x 1.965 GHz"}
+    # whole-step roofline: sum over convs of max(flops/peak, bytes/hbm)
+    roof_ms = sum(max(cv["flops"] / (useful_peak * 1e12), cv["bytes"] / (hbm * 1e9)) * 1e3 for cv in convs)
+    roof["step_roofline_ms"] = round(roof_ms, 3)
+    roof["step_frac"] = round(roof_ms / (t_ms / args.steps), 4)
+
+    layers_table = []
+    seen = {}
+    for cv, ms in zip(convs, per_conv_ms):
+        nm = cv["layer"].name
+        if nm in seen:
+            seen[nm]["ms"].append(ms)
+            continue
+        seen[nm] = {"layer": nm, "tuple": [cv["layer"].window, cv["layer"].stride, cv["layer"].rows,
+                                           cv["layer"].cols, cv["layer"].channels, cv["layer"].features],
+                    "batch": B, "algo": C.ALGO_NAMES[cv["algo"]], "ms": [ms], "flops": cv["flops"],
+                    "bytes": cv["bytes"]}
+        layers_table.append(seen[nm])
+    for r in layers_table:
+        t = statistics.mean(r["ms"])
+        r["us"] = round(1e3 * t, 2)
+        r["gflops"] = round(r["flops"] / (t / 1e3) / 1e9, 1)
+        r["gbs"] = round(r["bytes"] / (t / 1e3) / 1e9, 1)
+        rl = max(r["flops"] / (useful_peak * 1e12), r["bytes"] / (hbm * 1e9)) * 1e3
+        r["roofline_frac"] = round(rl / t, 3)
+        r["bound"] = "tensor" if r["flops"] / (useful_peak * 1e12) >= r["bytes"] / (hbm * 1e9) else "hbm"
+        r["count"] = len(r["ms"])
+        del r["ms"]
+
+    launches = sum(cv["launches"] for cv in convs) * args.steps
+
+    # ---- end to end through the public API: pinned host -> device, forward, device -> host
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, C, convs, ws, stream, world, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline()
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 3), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32" if math == C.MATH_FP32 else "tf32",
+                "data": "synthetic (seeded splitmix64 uniform[-1,1), device-generated)",
+                "config": workload_config(args, B), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk, "wall_s_timed": round(wall, 3),
+                "pct_of_peak": round(100 * value / 1e3 / (useful_peak * world), 2)}
+        if args.layers_out:
+            with open(args.layers_out, "w") as f:
+                json.dump({"bench": line, "layers": layers_table}, f, indent=1)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(args, C, convs, ws, stream, world, dev):
+    """Same metric through the public API with host buffers: every step copies each conv's input
+    from pinned host memory, runs conv2d_forward, and reads each output back to pinned host memory.
+    Copies and compute are pipelined over three streams (H2D, compute, D2H)."""
+    import torch
+    import torch.distributed as dist
+    # per distinct layer one pinned host input/output (the step still moves every conv's bytes)
+    host_in, host_out = {}, {}
+    for cv in convs:
+        nm = cv["layer"].name
+        if nm not in host_in:
+            host_in[nm] = torch.empty(cv["x"].numel(), dtype=torch.float32, pin_memory=True)
+            host_in[nm].copy_(cv["x"])
+            host_out[nm] = torch.empty(cv["y"].numel(), dtype=torch.float32, pin_memory=True)
+    s_h2d = torch.cuda.Stream()
+    s_d2h = torch.cuda.Stream()
+    h2d_bytes = sum(cv["x"].numel() * 4 for cv in convs)
+    d2h_bytes = sum(cv["y"].numel() * 4 for cv in convs)
+    # device staging: two input slots per size class would save memory; the resident buffers are reused
+    ev_in = [torch.cuda.Event() for _ in convs]
+    ev_done = [torch.cuda.Event() for _ in convs]
+
+    def e2e_step():
+        for i, cv in enumerate(convs):
+            with torch.cuda.stream(s_h2d):
+                if i > 0:
+                    s_h2d.wait_event(ev_done[i - 1])  # keep at most one conv of copies ahead
+                cv["x"].copy_(host_in[cv["layer"].name], non_blocking=True)
+                ev_in[i].record(s_h2d)
+            stream.wait_event(ev_in[i])
+            C.conv2d_forward(cv["p"], C.ALGO_AUTO, cv["x"], cv["w"], cv["y"], ws, ws.numel(), stream)
+            ev_done[i].record(stream)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev_done[i])
+                host_out[cv["layer"].name].copy_(cv["y"], non_blocking=True)
+        stream.wait_stream(s_d2h)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 3))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1)
+    tm = torch.tensor([t], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    t = float(tm.item())
+    flops = sum(cv["flops"] for cv in convs) * world * steps
+    return {"value": round(flops / (t / 1e3) / 1e9, 1), "unit": "GFLOP/s", "h2d_bytes_per_step": h2d_bytes,
+            "d2h_bytes_per_step": d2h_bytes, "steps": steps, "ms_per_step": round(t / steps, 3),
+            "path": "pinned host -> cudaMemcpyAsync -> conv2d_forward(AUTO) -> cudaMemcpyAsync -> pinned host, "
+                    "3 streams pipelined"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

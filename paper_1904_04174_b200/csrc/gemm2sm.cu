@@ -1,0 +1,498 @@
+// gemm2sm.cu -- persistent 2-CTA tcgen05 GEMM core (the contraction behind implicit GEMM,
+// 1x1-as-matmul and Winograd's batched GEMMs).
+//
+//   D[b](m, n) = sum_k A[b](m, k) * Bt[b](n, k)        fp32 in, fp32 accumulate in TMEM
+//
+// Design:
+//   * a CTA pair (cluster of 2, tcgen05 cta_group::2) owns a 256 x BN output tile: CTA r holds
+//     A rows [128r, 128r+128) and B rows (output features) [r*BN/2, (r+1)*BN/2) in its smem;
+//     the leader issues M=256 x N=BN x K=8 kind::tf32 MMAs that read both CTAs' smem and
+//     accumulate into both CTAs' TMEM (each CTA: its 128 rows x BN fp32 columns);
+//   * persistent: grid = min(tiles, 74) pairs, static round-robin tile schedule, two TMEM
+//     accumulators so the epilogue of tile i overlaps the main loop of tile i+1;
+//   * operands arrive by TMA into SWIZZLE_128B K-major stages:
+//       A_IM2COL : cp.async.bulk.tensor.4d.im2col straight from the NHWC input -- the im2col
+//                  matrix is never materialised; one box = 128 output
+//                  pixels x 32 channels at filter tap (r, s); OOB (padding, tails) -> zeros;
+//       A_DENSE  : 3-D tiled TMA of a dense K-major matrix (Winograd V, 1x1 fallbacks);
+//       A_GATHER : cp.async 16-byte gathers by the transform warps (C % 32 != 0, e.g. the
+//                  C=3 stem after channel padding to 4, flat k = (r, s, c));
+//     B (filter, pre-transposed/split by filter_prep) always by 3-D tiled TMA;
+//   * 3xTF32 (fp32-faithful mode): the transform warps split A in place into hi (low 13
+//     mantissa bits cleared) and lo = a - hi; B's split comes from filter_prep; the MMA warp
+//     issues lo*hi + hi*lo + hi*hi per K=8 step.
+// Warp roles (320 threads): 0-3 transform/gather, 4 TMA producer, 5 MMA issuer + TMEM
+// allocator, 6-9 epilogue (TMEM -> registers -> global, 32 columns per tcgen05.ld).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "gemm2sm.h"
+#include "sm100.cuh"
+
+namespace conv2d {
+namespace {
+
+using namespace sm100;
+
+constexpr int BMC = 128;  // rows per CTA (pair tile = 256)
+constexpr int BK = 32;    // fp32 per 128-byte swizzle row
+constexpr int NTHREADS = 320;
+constexpr int A_TILE = BMC * BK * 4;  // 16 KB
+
+struct DevArgs {
+  int H, W, C, KH, KW, SH, SW, HO, WO, PT, PL;
+  int ncb;
+  int Cg;
+  const float* xg;
+  int64_t Kg;
+  int64_t M, N;
+  int nkb, mt, nt, splits, batch, total_tiles;
+  float* d;
+  int64_t ldd, d_bstride;
+  float* partial;
+};
+
+template <int BN, bool THREE_X>
+struct Cfg {
+  static constexpr int BHALF = (BN / 2) * BK * 4;
+  static constexpr int STAGE = (THREE_X ? 2 : 1) * (A_TILE + BHALF);
+  static constexpr int BUDGET = 222 * 1024;
+  static constexpr int STAGES = (BUDGET / STAGE) > 8 ? 8 : (BUDGET / STAGE);
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 512;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulators
+};
+
+struct Tile {
+  int mi, ni, bz, split, kb0, kb1;
+};
+
+__device__ __forceinline__ Tile decode(const DevArgs& a, int t) {
+  Tile r;
+  r.ni = t % a.nt;
+  const int rest = t / a.nt;
+  r.mi = rest % a.mt;
+  const int z = rest / a.mt;
+  r.bz = z / a.splits;
+  r.split = z % a.splits;
+  r.kb0 = (int)((int64_t)r.split * a.nkb / a.splits);
+  r.kb1 = (int)((int64_t)(r.split + 1) * a.nkb / a.splits);
+  return r;
+}
+
+template <int BN, bool THREE_X, int AMODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    gemm2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
+                   const __grid_constant__ CUtensorMap tmBl, const __grid_constant__ DevArgs args) {
+  using C_ = Cfg<BN, THREE_X>;
+  constexpr int S = C_::STAGES;
+  constexpr int LAG = S - 1 < 3 ? S - 1 : 3;  // gather pipelining depth (cp.async groups in flight)
+  static_assert(S >= 2, "need >= 2 stages");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  auto a_hi = [&](int s) { return smem + (size_t)s * C_::STAGE; };
+  auto a_lo = [&](int s) { return smem + (size_t)s * C_::STAGE + A_TILE; };
+  auto b_hi = [&](int s) { return smem + (size_t)s * C_::STAGE + (THREE_X ? 2 : 1) * A_TILE; };
+  auto b_lo = [&](int s) { return smem + (size_t)s * C_::STAGE + 2 * A_TILE + C_::BHALF; };
+  uint64_t* ld_full = reinterpret_cast<uint64_t*>(smem + S * C_::STAGE);
+  uint64_t* full = ld_full + S;
+  uint64_t* empty = full + S;
+  uint64_t* tmem_full = empty + S;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cid = (int)cluster_id_x();
+  const int ncl = (int)nclusters_x();
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&ld_full[s], 1);
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 2);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 4 && lane == 0) {
+    if (AMODE != A_GATHER) tma_prefetch(&tmA);
+    tma_prefetch(&tmBh);
+    if (THREE_X) tma_prefetch(&tmBl);
+  }
+  if (warp == 5) tmem_alloc_2sm<C_::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 4) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      uint32_t it = 0;
+      const uint32_t bytes = (AMODE != A_GATHER ? A_TILE : 0) + (THREE_X ? 2 : 1) * C_::BHALF;
+      for (int t = cid; t < args.total_tiles; t += ncl) {
+        const Tile tl = decode(args, t);
+        const int64_t m_cta = (int64_t)tl.mi * 2 * BMC + rank * BMC;
+        int wb = 0, hb = 0, nimg = 0;
+        if (AMODE == A_IM2COL) {
+          const int64_t hw = (int64_t)args.HO * args.WO;
+          nimg = (int)(m_cta / hw);
+          const int rem = (int)(m_cta % hw);
+          wb = (rem % args.WO) * args.SW - args.PL;
+          hb = (rem / args.WO) * args.SH - args.PT;
+        }
+        const int nrow = tl.ni * BN + (int)rank * (BN / 2);
+        for (int kb = tl.kb0; kb < tl.kb1; ++kb, ++it) {
+          const int s = it % S;
+          const uint32_t u = it / S;
+          if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+          mbar_arrive_expect_tx(&ld_full[s], bytes);
+          if (AMODE == A_IM2COL) {
+            const int tap = kb / args.ncb;
+            const int cb = kb - tap * args.ncb;
+            tma_load_im2col_4d(&tmA, &ld_full[s], smem_u32(a_hi(s)), cb * BK, wb, hb, nimg,
+                               (uint16_t)(tap % args.KW), (uint16_t)(tap / args.KW));
+          } else if (AMODE == A_DENSE) {
+            tma_load_3d(&tmA, &ld_full[s], smem_u32(a_hi(s)), kb * BK, (int)m_cta, tl.bz);
+          }
+          tma_load_3d(&tmBh, &ld_full[s], smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
+          if (THREE_X) tma_load_3d(&tmBl, &ld_full[s], smem_u32(b_lo(s)), kb * BK, nrow, tl.bz);
+        }
+      }
+      // drain: every stage must be released before the CTA may exit (multicast commits target us)
+      for (int i = 0; i < S; ++i, ++it) {
+        const uint32_t u = it / S;
+        if (u > 0) mbar_wait(&empty[it % S], (u - 1) & 1);
+      }
+    }
+  } else if (warp == 5) {
+    // ============================ MMA issuer (leader CTA) ============================
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(2 * BMC, BN);
+      uint32_t it = 0, ai = 0;
+      for (int t = cid; t < args.total_tiles; t += ncl, ++ai) {
+        const Tile tl = decode(args, t);
+        const int acc = ai & 1;
+        const uint32_t ua = ai >> 1;
+        if (ua > 0) mbar_wait_cluster(&tmem_empty[acc], (ua - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = tl.kb0; kb < tl.kb1; ++kb, ++it) {
+          const int s = it % S;
+          mbar_wait_cluster(&full[s], (it / S) & 1);
+          tc_fence_after();
+          const uint64_t dah = umma_desc_sw128_kmajor(smem_u32(a_hi(s)));
+          const uint64_t dbh = umma_desc_sw128_kmajor(smem_u32(b_hi(s)));
+          const uint64_t dal = THREE_X ? umma_desc_sw128_kmajor(smem_u32(a_lo(s))) : 0;
+          const uint64_t dbl = THREE_X ? umma_desc_sw128_kmajor(smem_u32(b_lo(s))) : 0;
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);
+            const uint32_t accum = (kb > tl.kb0 || k > 0) ? 1u : 0u;
+            if (THREE_X) {
+              mma_tf32_2sm(d, dal + adv, dbh + adv, idesc, accum);
+              mma_tf32_2sm(d, dah + adv, dbl + adv, idesc, 1u);
+              mma_tf32_2sm(d, dah + adv, dbh + adv, idesc, 1u);
+            } else {
+              mma_tf32_2sm(d, dah + adv, dbh + adv, idesc, accum);
+            }
+          }
+          mma_commit_2sm_mc(&empty[s], 0x3);
+        }
+        mma_commit_2sm_mc(&tmem_full[acc], 0x3);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 4) {
+    // ============================ transform / gather (128 threads) ============================
+    const int t = threadIdx.x;
+    const int j = t & 7;    // 16-byte chunk within the 128-byte k-row
+    const int rb = t >> 3;  // rows rb + 16 i
+    const uint32_t full_leader = mapa(smem_u32(full), 0);  // full[0] in the leader CTA
+
+    auto finalize = [&](uint32_t jt) {
+      const int s = jt % S;
+      mbar_wait(&ld_full[s], (jt / S) & 1);
+      if (THREE_X) {
+        uint8_t* ah = a_hi(s);
+        uint8_t* al = a_lo(s);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t off = sw128_offset(rb + 16 * i, j);
+          const float4 v = *reinterpret_cast<const float4*>(ah + off);
+          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+          *reinterpret_cast<float4*>(ah + off) = h;
+          *reinterpret_cast<float4*>(al + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+      }
+      if (THREE_X || AMODE == A_GATHER) fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (t == 0) mbar_arrive_cluster(full_leader + (uint32_t)(s * sizeof(uint64_t)));
+    };
+
+    uint32_t it = 0;
+    for (int tt = cid; tt < args.total_tiles; tt += ncl) {
+      const Tile tl = decode(args, tt);
+      if (AMODE == A_GATHER) {
+        int ihb[8], iwb[8];
+        int64_t rbase[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int64_t m = (int64_t)tl.mi * 2 * BMC + rank * BMC + rb + 16 * i;
+          if (m < args.M) {
+            const int wo = (int)(m % args.WO);
+            const int64_t q = m / args.WO;
+            const int ho = (int)(q % args.HO);
+            const int64_t n = q / args.HO;
+            ihb[i] = ho * args.SH - args.PT;
+            iwb[i] = wo * args.SW - args.PL;
+            rbase[i] = n * args.H * args.W * args.Cg;
+          } else {
+            ihb[i] = -(1 << 28);
+            iwb[i] = 0;
+            rbase[i] = 0;
+          }
+        }
+        for (int kb = tl.kb0; kb < tl.kb1; ++kb, ++it) {
+          const int s = it % S;
+          const uint32_t u = it / S;
+          if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+          const uint32_t sa = smem_u32(a_hi(s));
+          const int k0 = kb * BK + j * 4;
+          const int c = k0 % args.Cg;
+          const int rs = k0 / args.Cg;
+          const int sx = rs % args.KW;
+          const int r = rs / args.KW;
+          const bool kv = k0 < args.Kg;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int ih = ihb[i] + r, iw = iwb[i] + sx;
+            const bool v = kv && ih >= 0 && ih < args.H && iw >= 0 && iw < args.W;
+            const float* src = v ? args.xg + rbase[i] + ((int64_t)ih * args.W + iw) * args.Cg + c : args.xg;
+            cp_async16(sa + sw128_offset(rb + 16 * i, j), src, v ? 16u : 0u);
+          }
+          cp_async_commit();
+          if (it >= (uint32_t)LAG) {
+            cp_async_wait<LAG>();
+            finalize(it - LAG);
+          }
+        }
+      } else {
+        for (int kb = tl.kb0; kb < tl.kb1; ++kb, ++it) finalize(it);
+      }
+    }
+    if (AMODE == A_GATHER) {
+      cp_async_wait<0>();
+      for (uint32_t jt = (it > (uint32_t)LAG ? it - LAG : 0); jt < it; ++jt) finalize(jt);
+    }
+  } else {
+    // ============================ epilogue (warps 6-9) ============================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const uint32_t tmem_empty_leader = mapa(smem_u32(tmem_empty), 0);
+    const bool vec_ok = (args.ldd % 4) == 0;
+    uint32_t ai = 0;
+    for (int t = cid; t < args.total_tiles; t += ncl, ++ai) {
+      const Tile tl = decode(args, t);
+      const int acc = ai & 1;
+      mbar_wait(&tmem_full[acc], (ai >> 1) & 1);
+      tc_fence_after();
+      const int64_t m = (int64_t)tl.mi * 2 * BMC + rank * BMC + q * 32 + lane;
+      float* D = args.splits == 1 ? args.d + (int64_t)tl.bz * args.d_bstride
+                                  : args.partial + ((int64_t)tl.split * args.batch + tl.bz) * args.M * args.ldd;
+      const int n0 = tl.ni * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+        if (m < args.M) {
+          float* dst = D + m * args.ldd + n0 + c0;
+          const int64_t nrem = args.N - (n0 + c0);
+          if (vec_ok && nrem >= 32) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              reinterpret_cast<float4*>(dst)[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              if (k < nrem) dst[k] = v[k];
+          }
+        }
+      }
+      tc_fence_before();
+      named_bar_sync(2, 128);
+      if (threadIdx.x == 6 * 32) mbar_arrive_cluster(tmem_empty_leader + (uint32_t)(acc * sizeof(uint64_t)));
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc_2sm<C_::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host: tensor maps
+PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
+PFN_cuTensorMapEncodeIm2col_v12000 g_encode_im2col = nullptr;
+int g_driver_version = 0;
+std::once_flag g_once;
+
+cudaError_t load_driver_fns() {
+  cudaError_t err = cudaSuccess;
+  std::call_once(g_once, [&]() {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode_tiled = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode_im2col = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(p);
+    cudaDriverGetVersion(&g_driver_version);
+  });
+  if (!g_encode_tiled || !g_encode_im2col) err = cudaErrorSymbolNotFound;
+  return err;
+}
+
+// 3-D tiled map over a K-major matrix stack [d2][d1][d0], box {32, box1, 1}, SWIZZLE_128B
+bool make_tiled_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t row_stride_elems,
+                   uint32_t box1) {
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {row_stride_elems * 4, row_stride_elems * 4 * d1};
+  cuuint32_t box[3] = {32, box1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool make_im2col(CUtensorMap* m, const Problem& p, const float* x) {
+  cuuint64_t dims[4] = {(cuuint64_t)p.C, (cuuint64_t)p.W, (cuuint64_t)p.H, (cuuint64_t)p.N};
+  cuuint64_t strides[3] = {(cuuint64_t)p.C * 4, (cuuint64_t)p.W * p.C * 4, (cuuint64_t)p.H * p.W * p.C * 4};
+  const int pb = (p.HO - 1) * p.SH + p.KH - p.H - p.pad_top;
+  const int pr = (p.WO - 1) * p.SW + p.KW - p.W - p.pad_left;
+  int lower[2] = {-p.pad_left, -p.pad_top};
+  int upper[2] = {pr - (p.KW - 1), pb - (p.KH - 1)};
+  cuuint32_t es[4] = {1, (cuuint32_t)p.SW, (cuuint32_t)p.SH, 1};
+  if (g_encode_im2col(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides, lower, upper, 32,
+                      BMC, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  // Same driver workaround CUTLASS applies to im2col descriptors of tensors < 128 KiB on drivers <= 13.1.
+  if (g_driver_version <= 13010 && (uint64_t)p.in_elems() * 4 < 131072)
+    reinterpret_cast<uint64_t*>(m)[1] &= ~(1ull << 21);
+  return true;
+}
+
+template <int BN, bool THREE_X, int AMODE>
+cudaError_t launch_t(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const DevArgs& args,
+                     int clusters, cudaStream_t s) {
+  using C_ = Cfg<BN, THREE_X>;
+  auto kern = gemm2sm_kernel<BN, THREE_X, AMODE>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  kern<<<dim3(2 * clusters), NTHREADS, C_::SMEM, s>>>(a, bh, bl, args);
+  return cudaGetLastError();
+}
+
+template <bool THREE_X, int AMODE>
+cudaError_t launch_bn(int bn, const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl,
+                      const DevArgs& args, int clusters, cudaStream_t s) {
+  switch (bn) {
+    case 64: return launch_t<64, THREE_X, AMODE>(a, bh, bl, args, clusters, s);
+    case 128: return launch_t<128, THREE_X, AMODE>(a, bh, bl, args, clusters, s);
+    case 256: return launch_t<256, THREE_X, AMODE>(a, bh, bl, args, clusters, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+int gemm2_choose_block_n(int64_t N) {
+  if (N <= 64) return 64;
+  if (N <= 128) return 128;
+  return 256;
+}
+
+int gemm2_choose_splits(int64_t M, int64_t N, int nkb, int batch, int block_n) {
+  const int64_t tiles = ((M + 255) / 256) * ((N + block_n - 1) / block_n) * batch;
+  if (tiles >= 74 || nkb < 8) return 1;
+  int64_t s = 74 / tiles;             // fill one wave of CTA pairs
+  if (s > nkb / 4) s = nkb / 4;       // keep >= 4 k-blocks per split
+  if (s > 16) s = 16;
+  return s < 1 ? 1 : (int)s;
+}
+
+bool gemm2_im2col_ok(const Problem& p) {
+  const int pb = (p.HO - 1) * p.SH + p.KH - p.H - p.pad_top;
+  const int pr = (p.WO - 1) * p.SW + p.KW - p.W - p.pad_left;
+  const int lo[2] = {-p.pad_left, -p.pad_top}, up[2] = {pr - (p.KW - 1), pb - (p.KH - 1)};
+  for (int i = 0; i < 2; ++i)
+    if (lo[i] < -128 || lo[i] > 127 || up[i] < -128 || up[i] > 127) return false;
+  return p.C % 32 == 0 && p.SH <= 8 && p.SW <= 8 && p.KH <= 65535 && p.KW <= 65535;
+}
+
+cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
+  cudaError_t e = load_driver_fns();
+  if (e != cudaSuccess) return e;
+  DevArgs a{};
+  a.H = p.H; a.W = p.W; a.C = p.C; a.KH = p.KH; a.KW = p.KW; a.SH = p.SH; a.SW = p.SW;
+  a.HO = p.HO; a.WO = p.WO; a.PT = p.pad_top; a.PL = p.pad_left;
+  a.ncb = (p.C + 31) / 32;
+  a.Cg = g.gather_c;
+  a.xg = g.gather_x;
+  a.Kg = (int64_t)p.KH * p.KW * g.gather_c;
+  a.M = g.M; a.N = g.N;
+  a.nkb = (int)(g.kpad / 32);
+  a.mt = (int)((g.M + 255) / 256);
+  a.nt = (int)((g.N + g.block_n - 1) / g.block_n);
+  a.splits = g.splits;
+  a.batch = g.batch;
+  const int64_t tiles = (int64_t)a.mt * a.nt * g.batch * g.splits;
+  if (tiles > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
+  a.total_tiles = (int)tiles;
+  a.d = g.d; a.ldd = g.ldd; a.d_bstride = g.d_batch_stride; a.partial = g.partial;
+
+  alignas(64) CUtensorMap ta{}, tbh{}, tbl{};
+  bool ok = true;
+  if (g.a_mode == A_IM2COL) ok = make_im2col(&ta, p, g.a);
+  else if (g.a_mode == A_DENSE) ok = make_tiled_3d(&ta, g.a, g.a_k, g.M, g.batch, g.lda, BMC);
+  ok = ok && make_tiled_3d(&tbh, g.bt_hi, g.kpad, g.npad, g.batch, g.kpad, g.block_n / 2);
+  if (g.three_x) ok = ok && make_tiled_3d(&tbl, g.bt_lo, g.kpad, g.npad, g.batch, g.kpad, g.block_n / 2);
+  if (!ok) return cudaErrorInvalidValue;
+  if (g.a_mode != A_IM2COL && g.a_mode != A_DENSE) ta = tbh;  // unused operand slot
+  if (!g.three_x) tbl = tbh;
+
+  const int clusters = (int)(tiles < 74 ? tiles : 74);
+  if (g.three_x) {
+    switch (g.a_mode) {
+      case A_IM2COL: e = launch_bn<true, A_IM2COL>(g.block_n, ta, tbh, tbl, a, clusters, s); break;
+      case A_DENSE: e = launch_bn<true, A_DENSE>(g.block_n, ta, tbh, tbl, a, clusters, s); break;
+      default: e = launch_bn<true, A_GATHER>(g.block_n, ta, tbh, tbl, a, clusters, s); break;
+    }
+  } else {
+    switch (g.a_mode) {
+      case A_IM2COL: e = launch_bn<false, A_IM2COL>(g.block_n, ta, tbh, tbl, a, clusters, s); break;
+      case A_DENSE: e = launch_bn<false, A_DENSE>(g.block_n, ta, tbh, tbl, a, clusters, s); break;
+      default: e = launch_bn<false, A_GATHER>(g.block_n, ta, tbh, tbl, a, clusters, s); break;
+    }
+  }
+  if (e != cudaSuccess) return e;
+  if (g.splits > 1) e = launch_split_reduce(g.partial, g.d, (int64_t)g.batch * g.M, g.N, g.ldd, g.splits, s);
+  return e;
+}
+
+}  // namespace conv2d

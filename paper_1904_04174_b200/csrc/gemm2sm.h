@@ -1,0 +1,42 @@
+// gemm2sm.h -- host interface of the persistent 2-CTA tcgen05 GEMM core (gemm2sm.cu).
+#pragma once
+#include "internal.h"
+
+namespace conv2d {
+
+enum { A_IM2COL = 0, A_DENSE = 1, A_GATHER = 2 };
+
+struct Gemm2Args {
+  int a_mode;              // A_IM2COL: a = NHWC input (C % 32 == 0), k = (r, s, c-block of 32)
+                           // A_DENSE : a = [batch][M][lda] K-major matrix, lda % 4 == 0
+                           // A_GATHER: gather_x = NHWC input with gather_c (% 4 == 0) channels, flat k
+  const float* a;
+  int64_t lda;
+  int64_t a_k;             // A_DENSE: extent of A's k dimension (elements beyond it read as zero)
+  const float* gather_x;
+  int gather_c;
+  const float* bt_hi;      // [batch][npad][kpad] K-major, zero padded (TF32 hi in 3xTF32 mode)
+  const float* bt_lo;      // same layout, lo parts (3xTF32 only)
+  int64_t kpad, npad;
+  float* d;                // [batch][M][ldd]
+  int64_t ldd, d_batch_stride;
+  float* partial;          // [splits][batch][M][ldd] when splits > 1
+  int64_t M, N;
+  int batch, splits, block_n;
+  bool three_x;
+};
+
+cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s);
+int gemm2_choose_block_n(int64_t N);
+int gemm2_choose_splits(int64_t M, int64_t N, int nkb, int batch, int block_n);
+bool gemm2_im2col_ok(const Problem& p);
+
+// gemm_common.cu
+// Bt[n][tap*cstride + c] = w[tap][c][n] (HWCF viewed as taps x C x F) for c < C, n < F, tap < taps;
+// zero elsewhere in the npad x kpad matrix.  bt_lo != null: split into TF32 hi / lo.
+cudaError_t launch_filter_prep2(const float* w, int taps, int C, int F, int cstride, int64_t kpad, int64_t npad,
+                                float* bt_hi, float* bt_lo, cudaStream_t s);
+// NHWC with C channels -> NHWC with Cp >= C channels (zeros in the new channels)
+cudaError_t launch_pad_channels(const float* x, int64_t pixels, int C, int Cp, float* xp, cudaStream_t s);
+
+}  // namespace conv2d

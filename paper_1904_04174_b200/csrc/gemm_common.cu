@@ -1,0 +1,88 @@
+// gemm_common.cu -- small CUDA-core helpers around the tensor-core GEMM core:
+//   filter_prep2   : HWCF filter -> K-major Bt (the B operand), TF32 hi/lo split in 3xTF32 mode
+//   pad_channels   : NHWC C -> Cp (zero channels) so 16-byte gathers stay aligned (C=3 stems)
+//   split_reduce   : deterministic fixed-order sum of split-K partial tiles
+#include "gemm2sm.h"
+#include "sm100.cuh"
+
+namespace conv2d {
+namespace {
+
+// One 32 (k) x 32 (n) destination tile per block.  Source rows of the 32 k's are read
+// coalesced (32 consecutive features), written transposed (32 consecutive k's).
+__global__ void filter_prep2_kernel(const float* __restrict__ w, int taps, int C, int F, int cstride, int64_t kpad,
+                                    int64_t npad, float* __restrict__ bt_hi, float* __restrict__ bt_lo) {
+  __shared__ float tile[32][33];
+  const int64_t k0 = (int64_t)blockIdx.x * 32, n0 = (int64_t)blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t k = k0 + r;
+    const int tap = (int)(k / cstride), c = (int)(k % cstride);
+    const int64_t n = n0 + threadIdx.x;
+    float v = 0.f;
+    if (tap < taps && c < C && n < F) v = w[((int64_t)tap * C + c) * F + n];
+    tile[r][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int64_t n = n0 + r, k = k0 + threadIdx.x;
+    if (n < npad && k < kpad) {
+      const float v = tile[threadIdx.x][r];
+      const float h = bt_lo ? sm100::tf32_hi(v) : v;
+      bt_hi[n * kpad + k] = h;
+      if (bt_lo) bt_lo[n * kpad + k] = v - h;
+    }
+  }
+}
+
+__global__ void pad_channels_kernel(const float* __restrict__ x, int64_t pixels, int C, int Cp,
+                                    float* __restrict__ xp) {
+  const int64_t total = pixels * Cp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t px = i / Cp;
+    const int c = (int)(i % Cp);
+    xp[i] = c < C ? x[px * C + c] : 0.f;
+  }
+}
+
+// d[i] = sum_{s=0..splits-1} partial[s][i] over a dense rows x ldd plane (ldd % 4 == 0),
+// fixed split order: deterministic.
+__global__ void split_reduce_kernel(const float* __restrict__ partial, float* __restrict__ d, int64_t plane4,
+                                    int splits) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 acc = reinterpret_cast<const float4*>(partial)[i];
+    for (int s = 1; s < splits; ++s) {
+      const float4 v = reinterpret_cast<const float4*>(partial)[s * plane4 + i];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(d)[i] = acc;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_filter_prep2(const float* w, int taps, int C, int F, int cstride, int64_t kpad, int64_t npad,
+                                float* bt_hi, float* bt_lo, cudaStream_t s) {
+  dim3 grid((unsigned)((kpad + 31) / 32), (unsigned)((npad + 31) / 32));
+  filter_prep2_kernel<<<grid, dim3(32, 8), 0, s>>>(w, taps, C, F, cstride, kpad, npad, bt_hi, bt_lo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pad_channels(const float* x, int64_t pixels, int C, int Cp, float* xp, cudaStream_t s) {
+  const int64_t total = pixels * Cp;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  pad_channels_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, pixels, C, Cp, xp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split_reduce(const float* partial, float* d, int64_t rows, int64_t cols, int64_t ldd, int splits,
+                                cudaStream_t s) {
+  if (ldd % 4 != 0 || cols != ldd) return cudaErrorInvalidValue;  // callers only split dense, 16B rows
+  const int64_t plane4 = rows * ldd / 4;
+  int64_t blocks = (plane4 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  split_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(partial, d, plane4, splits);
+  return cudaGetLastError();
+}
+
+}  // namespace conv2d

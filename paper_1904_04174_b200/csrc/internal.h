@@ -41,38 +41,8 @@ cudaError_t launch_winograd(const Problem& p, const float* in, const float* filt
 // ---- synth.cu
 cudaError_t launch_synth_fill(float* dst, uint64_t count, uint64_t key, uint64_t offset, int dist, cudaStream_t s);
 
-// Generic tcgen05 GEMM used by igemm and winograd (gemm_core.cuh instantiations live in igemm.cu).
-//   D[b][m][n] = sum_k A[b](m,k) * Bt[b](n,k)      (Bt is K-major: row n holds k contiguous)
-// A comes either from the im2col gather of an NHWC tensor (conv mode) or from a dense
-// K-major matrix (dense mode, Winograd batched GEMMs).
-struct GemmArgs {
-  // A operand
-  int a_mode;             // 0 = im2col of `in` (conv geometry from Problem), 1 = dense row-major [batch][M][lda]
-  const float* a;         // in (mode 0) or dense A
-  int64_t lda;            // dense mode row stride (floats), multiple of 4
-  int64_t a_batch_stride; // dense mode
-  // B operand, already split (hi, lo) and K-major, zero-padded to Kpad columns and Npad rows
-  const float* bt_hi;
-  const float* bt_lo;     // null in TF32 mode
-  int64_t ldb;            // = Kpad
-  int64_t b_batch_stride;
-  // D
-  float* d;
-  int64_t ldd;            // row stride of D (floats)
-  int64_t d_batch_stride;
-  float* partial;         // split-K partials [splits][batch][M][ldd] (nullptr if splits == 1)
-  int64_t M, N, K;        // logical sizes; K padded up to a multiple of 32 internally
-  int batch;
-  int splits;
-  bool three_x;           // 3xTF32
-  int block_n;            // 64, 128 or 256
-};
-cudaError_t launch_gemm(const Problem& conv, const GemmArgs& g, cudaStream_t s);
-int gemm_choose_block_n(int64_t N, bool three_x);
-int gemm_choose_splits(int64_t M, int64_t N, int64_t K, int batch, int block_n);
+// gemm_common.cu
 cudaError_t launch_split_reduce(const float* partial, float* d, int64_t rows, int64_t cols, int64_t ldd,
                                 int splits, cudaStream_t s);
-cudaError_t launch_filter_prep(const float* filt, int64_t K, int64_t F, int64_t kpad, int64_t npad, float* bt_hi,
-                               float* bt_lo, cudaStream_t s);
 
 }  // namespace conv2d

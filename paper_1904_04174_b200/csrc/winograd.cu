@@ -18,7 +18,7 @@
 // workspace (the GEMMs run on the tensor cores); the fused form is DESIGN.md "Next".
 // TF32 mode rounds U and V to TF32 with cvt.rna (reading R16); FP32 mode runs the GEMMs
 // in 3xTF32.
-#include "internal.h"
+#include "gemm2sm.h"
 #include "sm100.cuh"
 
 namespace conv2d {
@@ -172,10 +172,10 @@ WPlan make_wplan(const Problem& p) {
   w.TW = (p.WO + 1) / 2;
   w.T = (int64_t)p.N * w.TH * w.TW;
   w.cpad = round_up(p.C, 32);
-  w.block_n = gemm_choose_block_n(p.F, w.three_x);
+  w.block_n = gemm2_choose_block_n(p.F);
   w.fpad = round_up(p.F, w.block_n);
   w.ldm = round_up(p.F, 4);
-  w.splits = gemm_choose_splits(w.T, p.F, w.cpad, 16, w.block_n);
+  w.splits = gemm2_choose_splits(w.T, p.F, (int)(w.cpad / 32), 16, w.block_n);
   if (w.ldm != p.F) w.splits = 1;
   w.ut_bytes = round_up(16 * w.fpad * w.cpad * 4, 256);
   w.v_bytes = round_up(16 * w.T * w.cpad * 4, 256);
@@ -221,27 +221,26 @@ cudaError_t launch_winograd(const Problem& p, const float* in, const float* filt
                                                            w.T, w.cpad, V, w.three_x ? 0 : 1);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  GemmArgs g{};
-  g.a_mode = 1;
+  Gemm2Args g{};
+  g.a_mode = A_DENSE;
   g.a = V;
   g.lda = w.cpad;
-  g.a_batch_stride = w.T * w.cpad;
+  g.a_k = w.cpad;
   g.bt_hi = ut_hi;
   g.bt_lo = ut_lo;
-  g.ldb = w.cpad;
-  g.b_batch_stride = w.fpad * w.cpad;
+  g.kpad = w.cpad;
+  g.npad = w.fpad;
   g.d = Mw;
   g.ldd = w.ldm;
   g.d_batch_stride = w.T * w.ldm;
   g.partial = partial;
   g.M = w.T;
   g.N = p.F;
-  g.K = w.cpad;
   g.batch = 16;
   g.splits = w.splits;
   g.three_x = w.three_x;
   g.block_n = w.block_n;
-  e = launch_gemm(p, g, s);
+  e = launch_gemm2(p, g, s);
   if (e != cudaSuccess) return e;
   wino_output_kernel<<<grid_for(w.T * p.F), 256, 0, s>>>(Mw, w.T, w.ldm, p.F, p.HO, p.WO, w.TH, w.TW, out);
   return cudaGetLastError();

@@ -193,3 +193,15 @@ def test_fault_injection_is_detected(cuda_ok):
     y[0, 5, 5, 5] += 1e-2
     with pytest.raises(AssertionError):
         check_close(p, y, ref, den, C().ALGO_IMPLICIT_GEMM, "fault")
+
+
+def test_tf32_mma_reads_truncated_operands(cuda_ok):
+    """Hardware characterisation behind the 3xTF32 split (DESIGN.md "Math modes"): kind::tf32
+    MMAs ignore the low 13 mantissa bits of fp32 operands, so feeding raw fp32 (TF32 mode) and
+    pre-truncated fp32 must give bit-identical outputs."""
+    p = P(2, 16, 16, 64, 64, 3, 3, math=1)
+    x, w = make_inputs(p, layer_id=800)
+    xt = (x.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+    wt = (w.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
+    a = C().ALGO_IMPLICIT_GEMM
+    assert np.array_equal(gpu_conv(p, x, w, a), gpu_conv(p, xt, wt, a))
