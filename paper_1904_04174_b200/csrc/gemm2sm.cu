@@ -18,9 +18,10 @@
 //       A_GATHER : cp.async 16-byte gathers by the transform warps (C % 32 != 0, e.g. the
 //                  C=3 stem after channel padding to 4, flat k = (r, s, c));
 //     B (filter, pre-transposed/split by filter_prep) always by 3-D tiled TMA;
-//   * 3xTF32 (fp32-faithful mode): the transform warps split A in place into hi (low 13
-//     mantissa bits cleared) and lo = a - hi; B's split comes from filter_prep; the MMA warp
-//     issues lo*hi + hi*lo + hi*hi per K=8 step.
+//   * 3xTF32 (fp32-faithful mode): the transform warps write lo = a - trunc_tf32(a) next to
+//     each A stage (hi = the raw fp32 stage itself: the tensor core reads only its top 19
+//     bits); B's split comes from filter_prep; the MMA warp issues lo*hi + hi*lo + hi*hi
+//     per K=8 step.
 // Warp roles (320 threads): 0-3 transform/gather, 4 TMA producer, 5 MMA issuer + TMEM
 // allocator, 6-9 epilogue (TMEM -> registers -> global, 32 columns per tcgen05.ld).
 #include <cuda.h>
@@ -89,6 +90,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   constexpr int S = C_::STAGES;
   constexpr int LAG = S - 1 < 3 ? S - 1 : 3;  // gather pipelining depth (cp.async groups in flight)
   static_assert(S >= 2, "need >= 2 stages");
+  // RELAY: A passes through the transform warps (3xTF32 split or cp.async gather), which then
+  // signal the leader; otherwise the TMA engines signal the leader's full barrier directly.
+  constexpr bool RELAY = THREE_X || AMODE == A_GATHER;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -112,12 +116,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&ld_full[s], 1);
-      mbar_init(&full[s], 2);
+      mbar_init(&full[s], RELAY ? 2 * 128 : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], 2);
+      mbar_init(&tmem_empty[a], 2 * 128);
     }
     fence_mbar_init();
   }
@@ -135,6 +139,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   if (warp == 4) {
     // ============================ TMA producer ============================
     if (lane == 0) {
+      const uint32_t full_leader = mapa(smem_u32(full), 0);
       uint32_t it = 0;
       const uint32_t bytes = (AMODE != A_GATHER ? A_TILE : 0) + (THREE_X ? 2 : 1) * C_::BHALF;
       for (int t = cid; t < args.total_tiles; t += ncl) {
@@ -153,17 +158,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const int s = it % S;
           const uint32_t u = it / S;
           if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
-          mbar_arrive_expect_tx(&ld_full[s], bytes);
-          if (AMODE == A_IM2COL) {
-            const int tap = kb / args.ncb;
-            const int cb = kb - tap * args.ncb;
-            tma_load_im2col_4d(&tmA, &ld_full[s], smem_u32(a_hi(s)), cb * BK, wb, hb, nimg,
-                               (uint16_t)(tap % args.KW), (uint16_t)(tap / args.KW));
-          } else if (AMODE == A_DENSE) {
-            tma_load_3d(&tmA, &ld_full[s], smem_u32(a_hi(s)), kb * BK, (int)m_cta, tl.bz);
+          const int tap = AMODE == A_IM2COL ? kb / args.ncb : 0;
+          const int cb = AMODE == A_IM2COL ? kb - tap * args.ncb : 0;
+          if (RELAY) {
+            mbar_arrive_expect_tx(&ld_full[s], bytes);
+            if (AMODE == A_IM2COL)
+              tma_load_im2col_4d(&tmA, &ld_full[s], smem_u32(a_hi(s)), cb * BK, wb, hb, nimg,
+                                 (uint16_t)(tap % args.KW), (uint16_t)(tap / args.KW));
+            else if (AMODE == A_DENSE)
+              tma_load_3d(&tmA, &ld_full[s], smem_u32(a_hi(s)), kb * BK, (int)m_cta, tl.bz);
+            tma_load_3d(&tmBh, &ld_full[s], smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
+            if (THREE_X) tma_load_3d(&tmBl, &ld_full[s], smem_u32(b_lo(s)), kb * BK, nrow, tl.bz);
+          } else {
+            // both CTAs' bytes land on the leader's full[s]; only the leader arms it
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes);
+            const uint32_t fb = full_leader + (uint32_t)(s * sizeof(uint64_t));
+            if (AMODE == A_IM2COL)
+              tma_load_im2col_4d_2sm(&tmA, fb, smem_u32(a_hi(s)), cb * BK, wb, hb, nimg, (uint16_t)(tap % args.KW),
+                                     (uint16_t)(tap / args.KW));
+            else
+              tma_load_3d_2sm(&tmA, fb, smem_u32(a_hi(s)), kb * BK, (int)m_cta, tl.bz);
+            tma_load_3d_2sm(&tmBh, fb, smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
           }
-          tma_load_3d(&tmBh, &ld_full[s], smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
-          if (THREE_X) tma_load_3d(&tmBl, &ld_full[s], smem_u32(b_lo(s)), kb * BK, nrow, tl.bz);
         }
       }
       // drain: every stage must be released before the CTA may exit (multicast commits target us)
@@ -181,12 +197,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const Tile tl = decode(args, t);
         const int acc = ai & 1;
         const uint32_t ua = ai >> 1;
-        if (ua > 0) mbar_wait_cluster(&tmem_empty[acc], (ua - 1) & 1);
+        if (ua > 0) mbar_wait(&tmem_empty[acc], (ua - 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * BN);
         for (int kb = tl.kb0; kb < tl.kb1; ++kb, ++it) {
           const int s = it % S;
-          mbar_wait_cluster(&full[s], (it / S) & 1);
+          mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
           const uint64_t dah = umma_desc_sw128_kmajor(smem_u32(a_hi(s)));
           const uint64_t dbh = umma_desc_sw128_kmajor(smem_u32(b_hi(s)));
@@ -221,20 +237,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       const int s = jt % S;
       mbar_wait(&ld_full[s], (jt / S) & 1);
       if (THREE_X) {
-        uint8_t* ah = a_hi(s);
-        uint8_t* al = a_lo(s);
+        const uint32_t ah = smem_u32(a_hi(s));
+        const uint32_t al = smem_u32(a_lo(s));
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const uint32_t off = sw128_offset(rb + 16 * i, j);
-          const float4 v = *reinterpret_cast<const float4*>(ah + off);
-          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
-          *reinterpret_cast<float4*>(ah + off) = h;
-          *reinterpret_cast<float4*>(al + off) = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+          // hi stays in place as raw fp32: kind::tf32 MMAs read only the top 19 bits (truncation,
+          // pinned by tests/test_gpu_parity.py::test_tf32_mma_reads_truncated_operands)
+          const float4 v = lds128(ah + off);
+          sts128(al + off, make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z),
+                                       v.w - tf32_hi(v.w)));
         }
       }
-      if (THREE_X || AMODE == A_GATHER) fence_proxy_async_smem();
-      named_bar_sync(1, 128);
-      if (t == 0) mbar_arrive_cluster(full_leader + (uint32_t)(s * sizeof(uint64_t)));
+      fence_proxy_async_smem();
+      mbar_arrive_remote(full_leader + (uint32_t)(s * sizeof(uint64_t)));
     };
 
     uint32_t it = 0;
@@ -284,7 +300,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             finalize(it - LAG);
           }
         }
-      } else {
+      } else if (RELAY) {
         for (int kb = tl.kb0; kb < tl.kb1; ++kb, ++it) finalize(it);
       }
     }
@@ -326,8 +342,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
       }
       tc_fence_before();
-      named_bar_sync(2, 128);
-      if (threadIdx.x == 6 * 32) mbar_arrive_cluster(tmem_empty_leader + (uint32_t)(acc * sizeof(uint64_t)));
+      mbar_arrive_remote(tmem_empty_leader + (uint32_t)(acc * sizeof(uint64_t)));
     }
   }
 
