@@ -53,15 +53,17 @@ struct DevArgs {
   float* d;
   int64_t ldd, d_bstride;
   float* partial;
+  int tma_store;  // 1: epilogue stages 32x32 chunks in smem and writes them with TMA stores
 };
 
 template <int BN, bool THREE_X>
 struct Cfg {
   static constexpr int BHALF = (BN / 2) * BK * 4;
   static constexpr int STAGE = (THREE_X ? 2 : 1) * (A_TILE + BHALF);
-  static constexpr int BUDGET = 222 * 1024;
+  static constexpr int EPI = 4 * 2 * 32 * 128;  // 4 epilogue warps x 2 buffers x (32 rows x 128 B)
+  static constexpr int BUDGET = 232448 - EPI - 1024 - 512;
   static constexpr int STAGES = (BUDGET / STAGE) > 8 ? 8 : (BUDGET / STAGE);
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 512;
+  static constexpr int SMEM = STAGES * STAGE + EPI + 1024 + 512;
   static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulators
 };
 
@@ -85,7 +87,8 @@ __device__ __forceinline__ Tile decode(const DevArgs& a, int t) {
 template <int BN, bool THREE_X, int AMODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     gemm2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
-                   const __grid_constant__ CUtensorMap tmBl, const __grid_constant__ DevArgs args) {
+                   const __grid_constant__ CUtensorMap tmBl, const __grid_constant__ CUtensorMap tmD,
+                   const __grid_constant__ DevArgs args) {
   using C_ = Cfg<BN, THREE_X>;
   constexpr int S = C_::STAGES;
   constexpr int LAG = S - 1 < 3 ? S - 1 : 3;  // gather pipelining depth (cp.async groups in flight)
@@ -100,7 +103,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   auto a_lo = [&](int s) { return smem + (size_t)s * C_::STAGE + A_TILE; };
   auto b_hi = [&](int s) { return smem + (size_t)s * C_::STAGE + (THREE_X ? 2 : 1) * A_TILE; };
   auto b_lo = [&](int s) { return smem + (size_t)s * C_::STAGE + 2 * A_TILE + C_::BHALF; };
-  uint64_t* ld_full = reinterpret_cast<uint64_t*>(smem + S * C_::STAGE);
+  uint8_t* epi_smem = smem + S * C_::STAGE;  // 1024-aligned (STAGE is a multiple of 1024)
+  uint64_t* ld_full = reinterpret_cast<uint64_t*>(smem + S * C_::STAGE + C_::EPI);
   uint64_t* full = ld_full + S;
   uint64_t* empty = full + S;
   uint64_t* tmem_full = empty + S;
@@ -310,16 +314,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
   } else {
     // ============================ epilogue (warps 6-9) ============================
+    // Each warp owns TMEM lanes [32q, 32q+32) = 32 output rows.  Per 32-column chunk:
+    // tcgen05.ld (thread i <- row i, 32 columns) -> either a SWIZZLE_128B smem chunk stored by
+    // TMA (coalesced, asynchronous; double-buffered per warp) or direct 16-byte stores.
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const uint32_t tmem_empty_leader = mapa(smem_u32(tmem_empty), 0);
     const bool vec_ok = (args.ldd % 4) == 0;
-    uint32_t ai = 0;
+    const uint32_t ebuf = smem_u32(epi_smem) + (uint32_t)(q * 2 * 4096);
+    if (args.tma_store && lane == 0) tma_prefetch(&tmD);
+    uint32_t ai = 0, chunk = 0;
     for (int t = cid; t < args.total_tiles; t += ncl, ++ai) {
       const Tile tl = decode(args, t);
       const int acc = ai & 1;
       mbar_wait(&tmem_full[acc], (ai >> 1) & 1);
       tc_fence_after();
-      const int64_t m = (int64_t)tl.mi * 2 * BMC + rank * BMC + q * 32 + lane;
+      const int64_t row0 = (int64_t)tl.mi * 2 * BMC + rank * BMC + q * 32;
+      const int64_t m = row0 + lane;
+      const int z = args.splits == 1 ? tl.bz : tl.split * args.batch + tl.bz;
       float* D = args.splits == 1 ? args.d + (int64_t)tl.bz * args.d_bstride
                                   : args.partial + ((int64_t)tl.split * args.batch + tl.bz) * args.M * args.ldd;
       const int n0 = tl.ni * BN;
@@ -327,7 +338,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       for (int c0 = 0; c0 < BN; c0 += 32) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
-        if (m < args.M) {
+        if (c0 + 32 >= BN) {  // last TMEM read of this accumulator: hand it back to the MMA warp
+          tc_fence_before();
+          mbar_arrive_remote(tmem_empty_leader + (uint32_t)(acc * sizeof(uint64_t)));
+        }
+        if (args.tma_store) {
+          if (row0 < args.M && n0 + c0 < args.N) {
+            const uint32_t buf = ebuf + (chunk & 1) * 4096;
+            if (lane == 0) bulk_wait_read<1>();  // the store issued two chunks ago has read `buf`
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              sts128(buf + sw128_offset(lane, k), make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&tmD, buf, n0 + c0, (int)row0, z);
+              bulk_commit();
+            }
+            ++chunk;
+          }
+        } else if (m < args.M) {
           float* dst = D + m * args.ldd + n0 + c0;
           const int64_t nrem = args.N - (n0 + c0);
           if (vec_ok && nrem >= 32) {
@@ -341,9 +372,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive_remote(tmem_empty_leader + (uint32_t)(acc * sizeof(uint64_t)));
     }
+    if (args.tma_store && lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
@@ -409,8 +439,8 @@ bool make_im2col(CUtensorMap* m, const Problem& p, const float* x) {
 }
 
 template <int BN, bool THREE_X, int AMODE>
-cudaError_t launch_t(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const DevArgs& args,
-                     int clusters, cudaStream_t s) {
+cudaError_t launch_t(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& dm,
+                     const DevArgs& args, int clusters, cudaStream_t s) {
   using C_ = Cfg<BN, THREE_X>;
   auto kern = gemm2sm_kernel<BN, THREE_X, AMODE>;
   static bool attr = false;
@@ -419,17 +449,17 @@ cudaError_t launch_t(const CUtensorMap& a, const CUtensorMap& bh, const CUtensor
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<dim3(2 * clusters), NTHREADS, C_::SMEM, s>>>(a, bh, bl, args);
+  kern<<<dim3(2 * clusters), NTHREADS, C_::SMEM, s>>>(a, bh, bl, dm, args);
   return cudaGetLastError();
 }
 
 template <bool THREE_X, int AMODE>
 cudaError_t launch_bn(int bn, const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl,
-                      const DevArgs& args, int clusters, cudaStream_t s) {
+                      const CUtensorMap& dm, const DevArgs& args, int clusters, cudaStream_t s) {
   switch (bn) {
-    case 64: return launch_t<64, THREE_X, AMODE>(a, bh, bl, args, clusters, s);
-    case 128: return launch_t<128, THREE_X, AMODE>(a, bh, bl, args, clusters, s);
-    case 256: return launch_t<256, THREE_X, AMODE>(a, bh, bl, args, clusters, s);
+    case 64: return launch_t<64, THREE_X, AMODE>(a, bh, bl, dm, args, clusters, s);
+    case 128: return launch_t<128, THREE_X, AMODE>(a, bh, bl, dm, args, clusters, s);
+    case 256: return launch_t<256, THREE_X, AMODE>(a, bh, bl, dm, args, clusters, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -487,22 +517,40 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   else if (g.a_mode == A_DENSE) ok = make_tiled_3d(&ta, g.a, g.a_k, g.M, g.batch, g.lda, BMC);
   ok = ok && make_tiled_3d(&tbh, g.bt_hi, g.kpad, g.npad, g.batch, g.kpad, g.block_n / 2);
   if (g.three_x) ok = ok && make_tiled_3d(&tbl, g.bt_lo, g.kpad, g.npad, g.batch, g.kpad, g.block_n / 2);
+  // output tensor map: dims {N, M, planes} with row stride ldd; box 32 x 32, SWIZZLE_128B
+  alignas(64) CUtensorMap td{};
+  a.tma_store = 0;
+  if (ok && g.ldd % 4 == 0) {
+    float* dbase = g.splits == 1 ? g.d : g.partial;
+    const uint64_t planes = (uint64_t)g.batch * (g.splits == 1 ? 1 : g.splits);
+    const bool dense_batch = g.splits > 1 || g.batch == 1 || g.d_batch_stride == g.M * g.ldd;
+    if (dense_batch) {
+      cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, planes};
+      cuuint64_t strides[2] = {(cuuint64_t)g.ldd * 4, (cuuint64_t)g.ldd * 4 * g.M};
+      cuuint32_t box[3] = {32, 32, 1};
+      cuuint32_t es[3] = {1, 1, 1};
+      a.tma_store = g_encode_tiled(&td, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dbase, dims, strides, box, es,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+  }
   if (!ok) return cudaErrorInvalidValue;
+  if (!a.tma_store) td = tbh;  // unused slot
   if (g.a_mode != A_IM2COL && g.a_mode != A_DENSE) ta = tbh;  // unused operand slot
   if (!g.three_x) tbl = tbh;
 
   const int clusters = (int)(tiles < 74 ? tiles : 74);
   if (g.three_x) {
     switch (g.a_mode) {
-      case A_IM2COL: e = launch_bn<true, A_IM2COL>(g.block_n, ta, tbh, tbl, a, clusters, s); break;
-      case A_DENSE: e = launch_bn<true, A_DENSE>(g.block_n, ta, tbh, tbl, a, clusters, s); break;
-      default: e = launch_bn<true, A_GATHER>(g.block_n, ta, tbh, tbl, a, clusters, s); break;
+      case A_IM2COL: e = launch_bn<true, A_IM2COL>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
+      case A_DENSE: e = launch_bn<true, A_DENSE>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
+      default: e = launch_bn<true, A_GATHER>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
     }
   } else {
     switch (g.a_mode) {
-      case A_IM2COL: e = launch_bn<false, A_IM2COL>(g.block_n, ta, tbh, tbl, a, clusters, s); break;
-      case A_DENSE: e = launch_bn<false, A_DENSE>(g.block_n, ta, tbh, tbl, a, clusters, s); break;
-      default: e = launch_bn<false, A_GATHER>(g.block_n, ta, tbh, tbl, a, clusters, s); break;
+      case A_IM2COL: e = launch_bn<false, A_IM2COL>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
+      case A_DENSE: e = launch_bn<false, A_DENSE>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
+      default: e = launch_bn<false, A_GATHER>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
     }
   }
   if (e != cudaSuccess) return e;
