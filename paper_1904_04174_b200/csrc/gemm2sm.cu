@@ -50,6 +50,7 @@ struct DevArgs {
   int64_t Kg;
   int64_t M, N;
   int nkb, mt, nt, splits, batch, total_tiles;
+  int wblk, hblk;  // A_ROWSEG: 16-wide / 16-high spatial pair-tile grid
   float* d;
   int64_t ldd, d_bstride;
   float* partial;
@@ -144,13 +145,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     // ============================ TMA producer ============================
     if (lane == 0) {
       const uint32_t full_leader = mapa(smem_u32(full), 0);
+      // A_NARROW: k-block kb = 8 (tap, channel-quad) boxes of 128 px x 16 B, box q at +2 KB;
+      // taps past Kh*Kw get an out-of-image offset so the TMA zero-fills them.
+      const int nq = args.Cg / 4;
+      const int taps = args.KH * args.KW;
+      auto narrow_box = [&](int kb, int q, int& c, uint16_t& ow, uint16_t& oh) {
+        const int idx = kb * 8 + q;
+        const int tap = idx / nq;
+        c = (idx - tap * nq) * 4;
+        if (tap < taps) {
+          ow = (uint16_t)(tap % args.KW);
+          oh = (uint16_t)(tap / args.KW);
+        } else {
+          ow = 0xFFFF;
+          oh = 0xFFFF;
+          c = 0;
+        }
+      };
+      auto narrow_loads = [&](uint64_t* bar, uint32_t dst, int kb, int wb, int hb, int nimg) {
+#pragma unroll 1
+        for (int q = 0; q < 8; ++q) {
+          int c;
+          uint16_t ow, oh;
+          narrow_box(kb, q, c, ow, oh);
+          tma_load_im2col_4d(&tmA, bar, dst + q * 2048, c, wb, hb, nimg, ow, oh);
+        }
+      };
+      auto narrow_loads_2sm = [&](uint32_t bar, uint32_t dst, int kb, int wb, int hb, int nimg) {
+#pragma unroll 1
+        for (int q = 0; q < 8; ++q) {
+          int c;
+          uint16_t ow, oh;
+          narrow_box(kb, q, c, ow, oh);
+          tma_load_im2col_4d_2sm(&tmA, bar, dst + q * 2048, c, wb, hb, nimg, ow, oh);
+        }
+      };
       uint32_t it = 0;
       const uint32_t bytes = (AMODE != A_GATHER ? A_TILE : 0) + (THREE_X ? 2 : 1) * C_::BHALF;
       for (int t = cid; t < args.total_tiles; t += ncl) {
         const Tile tl = decode(args, t);
         const int64_t m_cta = (int64_t)tl.mi * 2 * BMC + rank * BMC;
         int wb = 0, hb = 0, nimg = 0;
-        if (AMODE == A_IM2COL) {
+        if (AMODE == A_ROWSEG) {
+          wb = (tl.mi % args.wblk) * 16;
+          hb = ((tl.mi / args.wblk) % args.hblk) * 16 + (int)rank * 8;
+          nimg = tl.mi / (args.wblk * args.hblk);
+        } else if (AMODE == A_IM2COL || AMODE == A_NARROW) {
           const int64_t hw = (int64_t)args.HO * args.WO;
           nimg = (int)(m_cta / hw);
           const int rem = (int)(m_cta % hw);
@@ -169,6 +209,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             if (AMODE == A_IM2COL)
               tma_load_im2col_4d(&tmA, &ld_full[s], smem_u32(a_hi(s)), cb * BK, wb, hb, nimg,
                                  (uint16_t)(tap % args.KW), (uint16_t)(tap / args.KW));
+            else if (AMODE == A_NARROW)
+              narrow_loads(&ld_full[s], smem_u32(a_hi(s)), kb, wb, hb, nimg);
+            else if (AMODE == A_ROWSEG)
+              tma_load_5d(&tmA, &ld_full[s], smem_u32(a_hi(s)), 0, wb, hb, nimg, kb);
             else if (AMODE == A_DENSE)
               tma_load_3d(&tmA, &ld_full[s], smem_u32(a_hi(s)), kb * BK, (int)m_cta, tl.bz);
             tma_load_3d(&tmBh, &ld_full[s], smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
@@ -180,6 +224,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             if (AMODE == A_IM2COL)
               tma_load_im2col_4d_2sm(&tmA, fb, smem_u32(a_hi(s)), cb * BK, wb, hb, nimg, (uint16_t)(tap % args.KW),
                                      (uint16_t)(tap / args.KW));
+            else if (AMODE == A_NARROW)
+              narrow_loads_2sm(fb, smem_u32(a_hi(s)), kb, wb, hb, nimg);
+            else if (AMODE == A_ROWSEG)
+              tma_load_5d_2sm(&tmA, fb, smem_u32(a_hi(s)), 0, wb, hb, nimg, kb);
             else
               tma_load_3d_2sm(&tmA, fb, smem_u32(a_hi(s)), kb * BK, (int)m_cta, tl.bz);
             tma_load_3d_2sm(&tmBh, fb, smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
@@ -208,20 +256,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const int s = it % S;
           mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
-          const uint64_t dah = umma_desc_sw128_kmajor(smem_u32(a_hi(s)));
+          const uint64_t dah = AMODE == A_NARROW ? umma_desc_interleave_kmajor(smem_u32(a_hi(s)), 2048, 128)
+                                                 : umma_desc_sw128_kmajor(smem_u32(a_hi(s)));
           const uint64_t dbh = umma_desc_sw128_kmajor(smem_u32(b_hi(s)));
-          const uint64_t dal = THREE_X ? umma_desc_sw128_kmajor(smem_u32(a_lo(s))) : 0;
+          const uint64_t dal = !THREE_X ? 0
+                               : AMODE == A_NARROW ? umma_desc_interleave_kmajor(smem_u32(a_lo(s)), 2048, 128)
+                                                   : umma_desc_sw128_kmajor(smem_u32(a_lo(s)));
           const uint64_t dbl = THREE_X ? umma_desc_sw128_kmajor(smem_u32(b_lo(s))) : 0;
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
             const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);
+            // narrow A: one K=8 step = two 16-byte core-matrix columns = 2 boxes = 4 KB
+            const uint64_t adv_a = AMODE == A_NARROW ? (uint64_t)((k * 4096) >> 4) : adv;
             const uint32_t accum = (kb > tl.kb0 || k > 0) ? 1u : 0u;
             if (THREE_X) {
-              mma_tf32_2sm(d, dal + adv, dbh + adv, idesc, accum);
-              mma_tf32_2sm(d, dah + adv, dbl + adv, idesc, 1u);
-              mma_tf32_2sm(d, dah + adv, dbh + adv, idesc, 1u);
+              mma_tf32_2sm(d, dal + adv_a, dbh + adv, idesc, accum);
+              mma_tf32_2sm(d, dah + adv_a, dbl + adv, idesc, 1u);
+              mma_tf32_2sm(d, dah + adv_a, dbh + adv, idesc, 1u);
             } else {
-              mma_tf32_2sm(d, dah + adv, dbh + adv, idesc, accum);
+              mma_tf32_2sm(d, dah + adv_a, dbh + adv, idesc, accum);
             }
           }
           mma_commit_2sm_mc(&empty[s], 0x3);
@@ -245,7 +298,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const uint32_t al = smem_u32(a_lo(s));
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const uint32_t off = sw128_offset(rb + 16 * i, j);
+          const uint32_t off = AMODE == A_NARROW ? (uint32_t)(t * 16 + i * 2048) : sw128_offset(rb + 16 * i, j);
           // hi stays in place as raw fp32: kind::tf32 MMAs read only the top 19 bits (truncation,
           // pinned by tests/test_gpu_parity.py::test_tf32_mma_reads_truncated_operands)
           const float4 v = lds128(ah + off);
@@ -328,8 +381,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       const int acc = ai & 1;
       mbar_wait(&tmem_full[acc], (ai >> 1) & 1);
       tc_fence_after();
-      const int64_t row0 = (int64_t)tl.mi * 2 * BMC + rank * BMC + q * 32;
-      const int64_t m = row0 + lane;
+      int64_t row0 = (int64_t)tl.mi * 2 * BMC + rank * BMC + q * 32;
+      int64_t m = row0 + lane;
+      int sw0 = 0, sh0 = 0, sn = 0;  // A_ROWSEG: this warp's 16 x 2 spatial block
+      if (AMODE == A_ROWSEG) {
+        sw0 = (tl.mi % args.wblk) * 16;
+        sh0 = ((tl.mi / args.wblk) % args.hblk) * 16 + (int)rank * 8 + 2 * q;
+        sn = tl.mi / (args.wblk * args.hblk);
+        const int ho = sh0 + lane / 16, wo = sw0 + lane % 16;
+        m = (ho < args.HO && wo < args.WO) ? ((int64_t)sn * args.HO + ho) * args.WO + wo : args.M;
+        row0 = (sh0 < args.HO && sw0 < args.WO) ? 0 : args.M;  // warp-uniform "any row valid"
+      }
       const int z = args.splits == 1 ? tl.bz : tl.split * args.batch + tl.bz;
       float* D = args.splits == 1 ? args.d + (int64_t)tl.bz * args.d_bstride
                                   : args.partial + ((int64_t)tl.split * args.batch + tl.bz) * args.M * args.ldd;
@@ -353,7 +415,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_3d(&tmD, buf, n0 + c0, (int)row0, z);
+              if (AMODE == A_ROWSEG) tma_store_4d(&tmD, buf, n0 + c0, sw0, sh0, sn);
+              else tma_store_3d(&tmD, buf, n0 + c0, (int)row0, z);
               bulk_commit();
             }
             ++chunk;
@@ -438,6 +501,37 @@ bool make_im2col(CUtensorMap* m, const Problem& p, const float* x) {
   return true;
 }
 
+bool make_im2col_narrow(CUtensorMap* m, const Problem& p, const float* x, int cg) {
+  cuuint64_t dims[4] = {(cuuint64_t)cg, (cuuint64_t)p.W, (cuuint64_t)p.H, (cuuint64_t)p.N};
+  cuuint64_t strides[3] = {(cuuint64_t)cg * 4, (cuuint64_t)p.W * cg * 4, (cuuint64_t)p.H * p.W * cg * 4};
+  const int pb = (p.HO - 1) * p.SH + p.KH - p.H - p.pad_top;
+  const int pr = (p.WO - 1) * p.SW + p.KW - p.W - p.pad_left;
+  int lower[2] = {-p.pad_left, -p.pad_top};
+  int upper[2] = {pr - (p.KW - 1), pb - (p.KH - 1)};
+  cuuint32_t es[4] = {1, (cuuint32_t)p.SW, (cuuint32_t)p.SH, 1};
+  if (g_encode_im2col(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(x), dims, strides, lower, upper, 4,
+                      BMC, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (g_driver_version <= 13010 && (uint64_t)p.N * p.H * p.W * cg * 4 < 131072)
+    reinterpret_cast<uint64_t*>(m)[1] &= ~(1ull << 21);
+  return true;
+}
+
+// A_ROWSEG: 5-D view {e, wo, ho, n, r} of the padded input xp (N, Hp, Wp, cg) with OVERLAPPING strides:
+// element (e, wo, ho, n, r) = xp[n][ho*SH + r][wo*SW + e / cg][e % cg]; e < KW*cg, box {32, 16, 8, 1, 1}.
+bool make_rowseg(CUtensorMap* m, const Problem& p, const float* xp, int cg, int hp, int wp) {
+  cuuint64_t dims[5] = {(cuuint64_t)p.KW * cg, (cuuint64_t)p.WO, (cuuint64_t)p.HO, (cuuint64_t)p.N,
+                        (cuuint64_t)p.KH};
+  cuuint64_t strides[4] = {(cuuint64_t)p.SW * cg * 4, (cuuint64_t)p.SH * wp * cg * 4, (cuuint64_t)hp * wp * cg * 4,
+                           (cuuint64_t)wp * cg * 4};
+  cuuint32_t box[5] = {32, 16, 8, 1, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(xp), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int BN, bool THREE_X, int AMODE>
 cudaError_t launch_t(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& dm,
                      const DevArgs& args, int clusters, cudaStream_t s) {
@@ -481,6 +575,22 @@ int gemm2_choose_splits(int64_t M, int64_t N, int nkb, int batch, int block_n) {
   return s < 1 ? 1 : (int)s;
 }
 
+static bool corners_ok(const Problem& p) {
+  const int pb = (p.HO - 1) * p.SH + p.KH - p.H - p.pad_top;
+  const int pr = (p.WO - 1) * p.SW + p.KW - p.W - p.pad_left;
+  const int lo[2] = {-p.pad_left, -p.pad_top}, up[2] = {pr - (p.KW - 1), pb - (p.KH - 1)};
+  for (int i = 0; i < 2; ++i)
+    if (lo[i] < -128 || lo[i] > 127 || up[i] < -128 || up[i] > 127) return false;
+  return p.SH <= 8 && p.SW <= 8 && p.W < 60000 && p.H < 60000;
+}
+
+bool gemm2_narrow_ok(const Problem& p) { return corners_ok(p); }
+
+bool gemm2_rowseg_ok(const Problem& p) {
+  const int cg = (p.C + 3) / 4 * 4;
+  return p.KW * cg <= 32 && p.C < 32 && p.KH <= 64;
+}
+
 bool gemm2_im2col_ok(const Problem& p) {
   const int pb = (p.HO - 1) * p.SH + p.KH - p.H - p.pad_top;
   const int pr = (p.WO - 1) * p.SW + p.KW - p.W - p.pad_left;
@@ -503,6 +613,11 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   a.M = g.M; a.N = g.N;
   a.nkb = (int)(g.kpad / 32);
   a.mt = (int)((g.M + 255) / 256);
+  if (g.a_mode == A_ROWSEG) {
+    a.wblk = (p.WO + 15) / 16;
+    a.hblk = (p.HO + 15) / 16;
+    a.mt = p.N * a.wblk * a.hblk;
+  }
   a.nt = (int)((g.N + g.block_n - 1) / g.block_n);
   a.splits = g.splits;
   a.batch = g.batch;
@@ -514,6 +629,8 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   alignas(64) CUtensorMap ta{}, tbh{}, tbl{};
   bool ok = true;
   if (g.a_mode == A_IM2COL) ok = make_im2col(&ta, p, g.a);
+  else if (g.a_mode == A_NARROW) ok = make_im2col_narrow(&ta, p, g.gather_x, g.gather_c);
+  else if (g.a_mode == A_ROWSEG) ok = make_rowseg(&ta, p, g.gather_x, g.gather_c, g.hp, g.wp);
   else if (g.a_mode == A_DENSE) ok = make_tiled_3d(&ta, g.a, g.a_k, g.M, g.batch, g.lda, BMC);
   ok = ok && make_tiled_3d(&tbh, g.bt_hi, g.kpad, g.npad, g.batch, g.kpad, g.block_n / 2);
   if (g.three_x) ok = ok && make_tiled_3d(&tbl, g.bt_lo, g.kpad, g.npad, g.batch, g.kpad, g.block_n / 2);
@@ -524,7 +641,16 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
     float* dbase = g.splits == 1 ? g.d : g.partial;
     const uint64_t planes = (uint64_t)g.batch * (g.splits == 1 ? 1 : g.splits);
     const bool dense_batch = g.splits > 1 || g.batch == 1 || g.d_batch_stride == g.M * g.ldd;
-    if (dense_batch) {
+    if (g.a_mode == A_ROWSEG) {
+      cuuint64_t dims[4] = {(cuuint64_t)g.N, (cuuint64_t)p.WO, (cuuint64_t)p.HO, (cuuint64_t)p.N};
+      cuuint64_t strides[3] = {(cuuint64_t)g.ldd * 4, (cuuint64_t)g.ldd * 4 * p.WO,
+                               (cuuint64_t)g.ldd * 4 * p.WO * p.HO};
+      cuuint32_t box[4] = {32, 16, 2, 1};
+      cuuint32_t es[4] = {1, 1, 1, 1};
+      a.tma_store = g_encode_tiled(&td, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, g.d, dims, strides, box, es,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    } else if (dense_batch) {
       cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, planes};
       cuuint64_t strides[2] = {(cuuint64_t)g.ldd * 4, (cuuint64_t)g.ldd * 4 * g.M};
       cuuint32_t box[3] = {32, 32, 1};
@@ -536,7 +662,7 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   }
   if (!ok) return cudaErrorInvalidValue;
   if (!a.tma_store) td = tbh;  // unused slot
-  if (g.a_mode != A_IM2COL && g.a_mode != A_DENSE) ta = tbh;  // unused operand slot
+  if (g.a_mode == A_GATHER) ta = tbh;  // unused operand slot
   if (!g.three_x) tbl = tbh;
 
   const int clusters = (int)(tiles < 74 ? tiles : 74);
@@ -544,12 +670,16 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
     switch (g.a_mode) {
       case A_IM2COL: e = launch_bn<true, A_IM2COL>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
       case A_DENSE: e = launch_bn<true, A_DENSE>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
+      case A_NARROW: e = launch_bn<true, A_NARROW>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
+      case A_ROWSEG: e = launch_bn<true, A_ROWSEG>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
       default: e = launch_bn<true, A_GATHER>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
     }
   } else {
     switch (g.a_mode) {
       case A_IM2COL: e = launch_bn<false, A_IM2COL>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
       case A_DENSE: e = launch_bn<false, A_DENSE>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
+      case A_NARROW: e = launch_bn<false, A_NARROW>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
+      case A_ROWSEG: e = launch_bn<false, A_ROWSEG>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
       default: e = launch_bn<false, A_GATHER>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
     }
   }

@@ -4,10 +4,16 @@
 
 namespace conv2d {
 
-enum { A_IM2COL = 0, A_DENSE = 1, A_GATHER = 2 };
+enum { A_IM2COL = 0, A_DENSE = 1, A_GATHER = 2, A_NARROW = 3, A_ROWSEG = 4 };
 
 struct Gemm2Args {
   int a_mode;              // A_IM2COL: a = NHWC input (C % 32 == 0), k = (r, s, c-block of 32)
+                           // A_NARROW: gather_x = NHWC input with gather_c (% 4 == 0) channels, flat k =
+                           //           (tap, channel quad): eight 128-px x 4-ch im2col boxes per k-block
+                           // A_ROWSEG: gather_x = spatially padded NHWC input (Hp x Wp x gather_c); one
+                           //           k-block per kernel row r holds the KW*gather_c contiguous floats of
+                           //           each output pixel (5-D tiled TMA over overlapping strides); the CTA
+                           //           tile is a 16 (wo) x 8 (ho) spatial block, the pair tile 16 x 16
                            // A_DENSE : a = [batch][M][lda] K-major matrix, lda % 4 == 0
                            // A_GATHER: gather_x = NHWC input with gather_c (% 4 == 0) channels, flat k
   const float* a;
@@ -24,18 +30,24 @@ struct Gemm2Args {
   int64_t M, N;
   int batch, splits, block_n;
   bool three_x;
+  int hp, wp;              // A_ROWSEG: padded input extent
 };
 
 cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s);
 int gemm2_choose_block_n(int64_t N);
 int gemm2_choose_splits(int64_t M, int64_t N, int nkb, int batch, int block_n);
 bool gemm2_im2col_ok(const Problem& p);
+bool gemm2_narrow_ok(const Problem& p);
+bool gemm2_rowseg_ok(const Problem& p);
 
 // gemm_common.cu
 // Bt[n][tap*cstride + c] = w[tap][c][n] (HWCF viewed as taps x C x F) for c < C, n < F, tap < taps;
 // zero elsewhere in the npad x kpad matrix.  bt_lo != null: split into TF32 hi / lo.
-cudaError_t launch_filter_prep2(const float* w, int taps, int C, int F, int cstride, int64_t kpad, int64_t npad,
-                                float* bt_hi, float* bt_lo, cudaStream_t s);
+// Bt[n][k] with k -> (r = k / rowstride, s = (k % rowstride) / cstride, c = k % cstride); zero padded
+cudaError_t launch_filter_prep2(const float* w, int KH, int KW, int C, int F, int cstride, int rowstride,
+                                int64_t kpad, int64_t npad, float* bt_hi, float* bt_lo, cudaStream_t s);
+cudaError_t launch_pad_spatial(const float* x, int N, int H, int W, int C, int Hp, int Wp, int Cp, int pt, int pl,
+                               float* xp, cudaStream_t s);
 // NHWC with C channels -> NHWC with Cp >= C channels (zeros in the new channels)
 cudaError_t launch_pad_channels(const float* x, int64_t pixels, int C, int Cp, float* xp, cudaStream_t s);
 

@@ -10,16 +10,20 @@ namespace {
 
 // One 32 (k) x 32 (n) destination tile per block.  Source rows of the 32 k's are read
 // coalesced (32 consecutive features), written transposed (32 consecutive k's).
-__global__ void filter_prep2_kernel(const float* __restrict__ w, int taps, int C, int F, int cstride, int64_t kpad,
-                                    int64_t npad, float* __restrict__ bt_hi, float* __restrict__ bt_lo) {
+// k -> (r = k / rowstride, e = k % rowstride, s = e / cstride, c = e % cstride); valid when
+// r < KH, s < KW, c < C.  Tap-major layouts use rowstride = KW * cstride.
+__global__ void filter_prep2_kernel(const float* __restrict__ w, int KH, int KW, int C, int F, int cstride,
+                                    int rowstride, int64_t kpad, int64_t npad, float* __restrict__ bt_hi,
+                                    float* __restrict__ bt_lo) {
   __shared__ float tile[32][33];
   const int64_t k0 = (int64_t)blockIdx.x * 32, n0 = (int64_t)blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
     const int64_t k = k0 + r;
-    const int tap = (int)(k / cstride), c = (int)(k % cstride);
+    const int kr = (int)(k / rowstride), e = (int)(k % rowstride);
+    const int ks = e / cstride, c = e % cstride;
     const int64_t n = n0 + threadIdx.x;
     float v = 0.f;
-    if (tap < taps && c < C && n < F) v = w[((int64_t)tap * C + c) * F + n];
+    if (kr < KH && ks < KW && c < C && n < F) v = w[((int64_t)(kr * KW + ks) * C + c) * F + n];
     tile[r][threadIdx.x] = v;
   }
   __syncthreads();
@@ -30,6 +34,29 @@ __global__ void filter_prep2_kernel(const float* __restrict__ w, int taps, int C
       const float h = bt_lo ? sm100::tf32_hi(v) : v;
       bt_hi[n * kpad + k] = h;
       if (bt_lo) bt_lo[n * kpad + k] = v - h;
+    }
+  }
+}
+
+// x (N,H,W,C) -> xp (N,Hp,Wp,Cp): xp[n][i][j][c] = x[n][i-pt][j-pl][c] inside the image and c < C, else 0.
+// One thread per padded pixel (32-bit index math), Cp/4 float4 stores each.
+__global__ void pad_spatial_kernel(const float* __restrict__ x, int N, int H, int W, int C, int Hp, int Wp, int Cp,
+                                   int pt, int pl, float* __restrict__ xp) {
+  const int total = N * Hp * Wp;
+  for (int px = blockIdx.x * blockDim.x + threadIdx.x; px < total; px += gridDim.x * blockDim.x) {
+    const int j = px % Wp;
+    const int q = px / Wp;
+    const int ii = q % Hp;
+    const int n = q / Hp;
+    const int ih = ii - pt, iw = j - pl;
+    const bool in = ih >= 0 && ih < H && iw >= 0 && iw < W;
+    const float* src = x + (((int64_t)n * H + ih) * W + iw) * C;
+    float4* dst = reinterpret_cast<float4*>(xp + (int64_t)px * Cp);
+    for (int c4 = 0; c4 < Cp; c4 += 4) {
+      float v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = (in && c4 + k < C) ? __ldg(src + c4 + k) : 0.f;
+      dst[c4 / 4] = make_float4(v[0], v[1], v[2], v[3]);
     }
   }
 }
@@ -60,10 +87,20 @@ __global__ void split_reduce_kernel(const float* __restrict__ partial, float* __
 
 }  // namespace
 
-cudaError_t launch_filter_prep2(const float* w, int taps, int C, int F, int cstride, int64_t kpad, int64_t npad,
-                                float* bt_hi, float* bt_lo, cudaStream_t s) {
+cudaError_t launch_filter_prep2(const float* w, int KH, int KW, int C, int F, int cstride, int rowstride,
+                                int64_t kpad, int64_t npad, float* bt_hi, float* bt_lo, cudaStream_t s) {
   dim3 grid((unsigned)((kpad + 31) / 32), (unsigned)((npad + 31) / 32));
-  filter_prep2_kernel<<<grid, dim3(32, 8), 0, s>>>(w, taps, C, F, cstride, kpad, npad, bt_hi, bt_lo);
+  filter_prep2_kernel<<<grid, dim3(32, 8), 0, s>>>(w, KH, KW, C, F, cstride, rowstride, kpad, npad, bt_hi, bt_lo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pad_spatial(const float* x, int N, int H, int W, int C, int Hp, int Wp, int Cp, int pt, int pl,
+                               float* xp, cudaStream_t s) {
+  const int64_t total = (int64_t)N * Hp * Wp;
+  if (total > 0x7FFFFFFF) return cudaErrorInvalidValue;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  pad_spatial_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, N, H, W, C, Hp, Wp, Cp, pt, pl, xp);
   return cudaGetLastError();
 }
 

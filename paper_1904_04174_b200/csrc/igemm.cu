@@ -11,6 +11,9 @@
 //   filter_prep2    W (HWCF) -> Bt (Fpad x Kpad, K-major), TF32 hi/lo split in FP32 mode
 //   gemm2sm         persistent 2-CTA tcgen05 GEMM
 //   [split_reduce]  when the pair-tile count is below one wave
+#include <cstdio>
+#include <cstdlib>
+
 #include "gemm2sm.h"
 
 namespace conv2d {
@@ -21,7 +24,7 @@ inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 struct Plan {
   int a_mode;
   bool three_x, pad;
-  int block_n, splits, cstride, cg;
+  int block_n, splits, cstride, cg, rowstride, hp, wp;
   int64_t kpad, npad;
   size_t bt_bytes, pad_bytes, partial_bytes, total;
 };
@@ -39,16 +42,33 @@ Plan make_plan(const Problem& p, bool is_1x1) {
   } else if (gemm2_im2col_ok(p)) {
     pl.a_mode = A_IM2COL;
     pl.cstride = p.C;  // C % 32 == 0: one tap = C/32 whole k-blocks
+  } else if (gemm2_rowseg_ok(p)) {
+    pl.a_mode = A_ROWSEG;  // small C, narrow windows (the C=3 stems): one 128-B row per pixel per kernel row
+    pl.cg = (int)round_up(p.C, 4);
+    pl.pad = true;         // spatial + channel padding pass
+    pl.cstride = pl.cg;
+    pl.rowstride = 32;
+    pl.hp = (p.HO - 1) * p.SH + p.KH;
+    pl.wp = (p.WO - 1) * p.SW + p.KW;
+  } else if (p.C <= 32 && gemm2_narrow_ok(p)) {
+    pl.a_mode = A_NARROW;  // small C (e.g. the C=3 stems): 4-channel im2col boxes, flat k
+    pl.cg = (int)round_up(p.C, 4);
+    pl.pad = pl.cg != p.C;
+    pl.cstride = pl.cg;
   } else {
     pl.a_mode = A_GATHER;
     pl.cg = (int)round_up(p.C, 4);
     pl.pad = pl.cg != p.C;
     pl.cstride = pl.cg;
   }
-  pl.kpad = round_up((int64_t)p.KH * p.KW * pl.cstride, 32);
-  pl.splits = (p.F % 4 == 0) ? gemm2_choose_splits(p.M(), p.F, (int)(pl.kpad / 32), 1, pl.block_n) : 1;
+  if (pl.a_mode != A_ROWSEG) pl.rowstride = p.KW * pl.cstride;
+  pl.kpad = pl.a_mode == A_ROWSEG ? (int64_t)p.KH * 32 : round_up((int64_t)p.KH * p.KW * pl.cstride, 32);
+  pl.splits = (p.F % 4 == 0 && pl.a_mode != A_ROWSEG)
+                  ? gemm2_choose_splits(p.M(), p.F, (int)(pl.kpad / 32), 1, pl.block_n) : 1;
   pl.bt_bytes = round_up((int64_t)pl.npad * pl.kpad * 4, 256);
-  pl.pad_bytes = pl.pad ? round_up((int64_t)p.N * p.H * p.W * pl.cg * 4, 256) : 0;
+  pl.pad_bytes = !pl.pad ? 0
+                 : pl.a_mode == A_ROWSEG ? round_up((int64_t)p.N * pl.hp * pl.wp * pl.cg * 4, 256)
+                                         : round_up((int64_t)p.N * p.H * p.W * pl.cg * 4, 256);
   pl.partial_bytes = pl.splits > 1 ? (size_t)pl.splits * p.M() * p.F * 4 : 0;
   pl.total = pl.bt_bytes * (pl.three_x ? 2 : 1) + pl.pad_bytes + pl.partial_bytes;
   return pl;
@@ -65,6 +85,11 @@ int igemm_launches(const Problem& p, bool is_1x1) {
 cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const float* filt, float* out, void* ws,
                          cudaStream_t s) {
   const Plan pl = make_plan(p, is_1x1);
+  static const bool debug = getenv("CONV2D_DEBUG") != nullptr;
+  if (debug)
+    fprintf(stderr, "[conv2d] igemm N=%d H=%d W=%d C=%d F=%d K=%dx%d S=%d: a_mode=%d bn=%d splits=%d kpad=%lld 3x=%d\n",
+            p.N, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH, pl.a_mode, pl.block_n, pl.splits, (long long)pl.kpad,
+            (int)pl.three_x);
   uint8_t* w8 = static_cast<uint8_t*>(ws);
   float* bt_hi = reinterpret_cast<float*>(w8);
   w8 += pl.bt_bytes;
@@ -77,12 +102,15 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
   if (pl.pad) {
     float* xp = reinterpret_cast<float*>(w8);
     w8 += pl.pad_bytes;
-    cudaError_t e = launch_pad_channels(in, (int64_t)p.N * p.H * p.W, p.C, pl.cg, xp, s);
+    cudaError_t e = pl.a_mode == A_ROWSEG
+                        ? launch_pad_spatial(in, p.N, p.H, p.W, p.C, pl.hp, pl.wp, pl.cg, p.pad_top, p.pad_left, xp, s)
+                        : launch_pad_channels(in, (int64_t)p.N * p.H * p.W, p.C, pl.cg, xp, s);
     if (e != cudaSuccess) return e;
     xg = xp;
   }
   float* partial = pl.splits > 1 ? reinterpret_cast<float*>(w8) : nullptr;
-  cudaError_t e = launch_filter_prep2(filt, p.KH * p.KW, p.C, p.F, pl.cstride, pl.kpad, pl.npad, bt_hi, bt_lo, s);
+  cudaError_t e =
+      launch_filter_prep2(filt, p.KH, p.KW, p.C, p.F, pl.cstride, pl.rowstride, pl.kpad, pl.npad, bt_hi, bt_lo, s);
   if (e != cudaSuccess) return e;
   Gemm2Args g{};
   g.a_mode = pl.a_mode;
@@ -105,6 +133,8 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
   g.splits = pl.splits;
   g.block_n = pl.block_n;
   g.three_x = pl.three_x;
+  g.hp = pl.hp;
+  g.wp = pl.wp;
   return launch_gemm2(p, g, s);
 }
 
