@@ -306,28 +306,33 @@ def main():
     tf32_peak = peaks["bf16_tflops"] / 2.0             # nominal TF32 : BF16 = 1 : 2 (B200_PROFILING.md)
     useful_peak = tf32_peak / 3.0 if math == C.MATH_FP32 else tf32_peak  # 3 MMAs per product in 3xTF32
     hbm = peaks["hbm_gbs"]
-    groups = {}
-    for cv, ms in zip(convs, per_conv_ms):
-        g = groups.setdefault(cv["algo"], {"ms": 0.0, "flops": 0, "bytes": 0, "n": 0})
-        g["ms"] += ms
-        g["flops"] += cv["flops"]
-        g["bytes"] += cv["bytes"]
-        g["n"] += 1
-    dom = max(groups, key=lambda a: groups[a]["ms"])
-    gd = groups[dom]
-    if dom in (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1, C.ALGO_WINOGRAD_F2X2_3X3):
-        ach = gd["flops"] / (gd["ms"] / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(useful_peak, 1), "unit": "TFLOP/s",
-                "frac": round(ach / useful_peak, 4), "traffic": None,
-                "kernel": f"conv2d_forward[{C.ALGO_NAMES[dom]}] (filter prep + tcgen05 GEMM + split reduce), "
-                          f"{gd['n']} of {len(convs)} convs, {100 * gd['ms'] / sum(per_conv_ms):.1f}% of step",
-                "peak_source": f"{peak_src} bf16 burst {peaks['bf16_tflops']} TF/s /2 (TF32)"
-                               + (" /3 (3xTF32 useful)" if math == C.MATH_FP32 else "")}
-    else:
-        ach = gd["flops"] / (gd["ms"] / 1e3) / 1e12
-        roof = {"bound": "alu", "achieved": round(ach, 2), "peak": round(148 * 128 * 2 * 1.965e9 / 1e12, 1),
-                "unit": "TFLOP/s", "frac": round(ach / (148 * 128 * 2 * 1.965e-3), 4), "traffic": None,
-                "kernel": f"conv2d_forward[{C.ALGO_NAMES[dom]}]", "peak_source": "148 SM x 128 FFMA x 2 x 1.965 GHz"}
+    # dominant kernel = the tcgen05 GEMM core (gemm2sm_kernel), which runs every conv whose chosen
+    # algorithm is implicit_gemm / matmul_1x1 / winograd; its per-conv time (CUDA events on the
+    # launching stream, inside the timed region) includes the small filter-prep / split-reduce launches.
+    tensor_algos = (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1, C.ALGO_WINOGRAD_F2X2_3X3)
+    grp = [(cv, ms) for cv, ms in zip(convs, per_conv_ms) if cv["algo"] in tensor_algos]
+    if not grp:  # degenerate: everything picked a CUDA-core algorithm
+        grp = list(zip(convs, per_conv_ms))
+    g_ms = sum(ms for _, ms in grp)
+    g_flops = sum(cv["flops"] for cv, _ in grp)
+    g_bytes = sum(cv["bytes"] for cv, _ in grp)
+    ach = g_flops / (g_ms / 1e3) / 1e12
+    traffic, traffic_src = None, None
+    tpath = os.path.join(ROOT, "profiles", "round1_step_traffic.json")
+    if os.path.exists(tpath) and world == 1 and math == C.MATH_FP32:
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        if tj.get("gemm_launches"):
+            traffic = round(tj["gemm_dram_bytes"] / tj["gemm_launches"] / 1e6, 2)
+            traffic_src = (f"MB per gemm2sm launch, ncu dram__bytes_read.sum+write.sum over one timed step "
+                           f"({tj['gemm_launches']} launches; profiles/round1_ncu.md)")
+    roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(useful_peak, 1), "unit": "TFLOP/s",
+            "frac": round(ach / useful_peak, 4), "traffic": traffic,
+            "traffic_unit": traffic_src, "algorithmic_mb_per_launch": round(g_bytes / len(grp) / 1e6, 2),
+            "kernel": f"gemm2sm_kernel (persistent 2-CTA tcgen05 GEMM) via conv2d_forward[implicit_gemm|matmul_1x1|"
+                      f"winograd]: {len(grp)} of {len(convs)} convs, {100 * g_ms / sum(per_conv_ms):.1f}% of step",
+            "peak_source": f"{peak_src} bf16 burst {peaks['bf16_tflops']} TF/s /2 (TF32)"
+                           + (" /3 (3xTF32 useful flops)" if math == C.MATH_FP32 else "")}
     # whole-step roofline: sum over convs of max(flops/peak, bytes/hbm)
     roof_ms = sum(max(cv["flops"] / (useful_peak * 1e12), cv["bytes"] / (hbm * 1e9)) * 1e3 for cv in convs)
     roof["step_roofline_ms"] = round(roof_ms, 3)
