@@ -60,11 +60,14 @@ struct DevArgs {
 template <int BN, bool THREE_X>
 struct Cfg {
   static constexpr int BHALF = (BN / 2) * BK * 4;
-  static constexpr int STAGE = (THREE_X ? 2 : 1) * (A_TILE + BHALF);
+  // TMA ring stage: [A (raw fp32 = TF32 hi) | B_hi | B_lo (3xTF32)]; in 3xTF32 the A lo halves live in a
+  // separate, shallower ring so the TMA ring can run deeper (latency hiding for small-N tiles).
+  static constexpr int STAGE = A_TILE + (THREE_X ? 2 : 1) * BHALF;
+  static constexpr int SL = THREE_X ? (BN == 128 ? 2 : 3) : 0;
   static constexpr int EPI = 4 * 2 * 32 * 128;  // 4 epilogue warps x 2 buffers x (32 rows x 128 B)
-  static constexpr int BUDGET = 232448 - EPI - 1024 - 512;
-  static constexpr int STAGES = (BUDGET / STAGE) > 8 ? 8 : (BUDGET / STAGE);
-  static constexpr int SMEM = STAGES * STAGE + EPI + 1024 + 512;
+  static constexpr int BUDGET = 232448 - EPI - 1024 - 512 - SL * A_TILE;
+  static constexpr int STAGES = (BUDGET / STAGE) > 12 ? 12 : (BUDGET / STAGE);
+  static constexpr int SMEM = STAGES * STAGE + SL * A_TILE + EPI + 1024 + 512;
   static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulators
 };
 
@@ -92,7 +95,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                    const __grid_constant__ DevArgs args) {
   using C_ = Cfg<BN, THREE_X>;
   constexpr int S = C_::STAGES;
-  constexpr int LAG = S - 1 < 3 ? S - 1 : 3;  // gather pipelining depth (cp.async groups in flight)
+  constexpr int LAG = S - 1 < 6 ? S - 1 : 6;  // gather pipelining depth (cp.async groups in flight)
   static_assert(S >= 2, "need >= 2 stages");
   // RELAY: A passes through the transform warps (3xTF32 split or cp.async gather), which then
   // signal the leader; otherwise the TMA engines signal the leader's full barrier directly.
@@ -100,15 +103,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int SL = C_::SL;
   auto a_hi = [&](int s) { return smem + (size_t)s * C_::STAGE; };
-  auto a_lo = [&](int s) { return smem + (size_t)s * C_::STAGE + A_TILE; };
-  auto b_hi = [&](int s) { return smem + (size_t)s * C_::STAGE + (THREE_X ? 2 : 1) * A_TILE; };
-  auto b_lo = [&](int s) { return smem + (size_t)s * C_::STAGE + 2 * A_TILE + C_::BHALF; };
-  uint8_t* epi_smem = smem + S * C_::STAGE;  // 1024-aligned (STAGE is a multiple of 1024)
-  uint64_t* ld_full = reinterpret_cast<uint64_t*>(smem + S * C_::STAGE + C_::EPI);
+  auto b_hi = [&](int s) { return smem + (size_t)s * C_::STAGE + A_TILE; };
+  auto b_lo = [&](int s) { return smem + (size_t)s * C_::STAGE + A_TILE + C_::BHALF; };
+  auto a_lo = [&](int l) { return smem + (size_t)S * C_::STAGE + (size_t)l * A_TILE; };  // lo ring slot
+  uint8_t* epi_smem = smem + S * C_::STAGE + SL * A_TILE;  // 1024-aligned (all sizes multiples of 1024)
+  uint64_t* ld_full = reinterpret_cast<uint64_t*>(epi_smem + C_::EPI);
   uint64_t* full = ld_full + S;
   uint64_t* empty = full + S;
-  uint64_t* tmem_full = empty + S;
+  uint64_t* lo_empty = empty + S;
+  uint64_t* tmem_full = lo_empty + (SL > 0 ? SL : 1);
   uint64_t* tmem_empty = tmem_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
@@ -124,6 +129,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       mbar_init(&full[s], RELAY ? 2 * 128 : 1);
       mbar_init(&empty[s], 1);
     }
+    for (int l = 0; l < SL; ++l) mbar_init(&lo_empty[l], 1);
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
       mbar_init(&tmem_empty[a], 2 * 128);
@@ -242,7 +248,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
   } else if (warp == 5) {
     // ============================ MMA issuer (leader CTA) ============================
-    if (rank == 0 && lane == 0) {
+    if (rank == 0) {  // whole warp, converged: operands stay warp-uniform
       constexpr uint32_t idesc = idesc_tf32(2 * BMC, BN);
       uint32_t it = 0, ai = 0;
       for (int t = cid; t < args.total_tiles; t += ncl, ++ai) {
@@ -259,9 +265,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const uint64_t dah = AMODE == A_NARROW ? umma_desc_interleave_kmajor(smem_u32(a_hi(s)), 2048, 128)
                                                  : umma_desc_sw128_kmajor(smem_u32(a_hi(s)));
           const uint64_t dbh = umma_desc_sw128_kmajor(smem_u32(b_hi(s)));
+          const int l = THREE_X ? (int)(it % SL) : 0;
           const uint64_t dal = !THREE_X ? 0
-                               : AMODE == A_NARROW ? umma_desc_interleave_kmajor(smem_u32(a_lo(s)), 2048, 128)
-                                                   : umma_desc_sw128_kmajor(smem_u32(a_lo(s)));
+                               : AMODE == A_NARROW ? umma_desc_interleave_kmajor(smem_u32(a_lo(l)), 2048, 128)
+                                                   : umma_desc_sw128_kmajor(smem_u32(a_lo(l)));
           const uint64_t dbl = THREE_X ? umma_desc_sw128_kmajor(smem_u32(b_lo(s))) : 0;
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
@@ -270,16 +277,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             const uint64_t adv_a = AMODE == A_NARROW ? (uint64_t)((k * 4096) >> 4) : adv;
             const uint32_t accum = (kb > tl.kb0 || k > 0) ? 1u : 0u;
             if (THREE_X) {
-              mma_tf32_2sm(d, dal + adv_a, dbh + adv, idesc, accum);
-              mma_tf32_2sm(d, dah + adv_a, dbl + adv, idesc, 1u);
-              mma_tf32_2sm(d, dah + adv_a, dbh + adv, idesc, 1u);
+              mma_tf32_2sm_warp(d, dal + adv_a, dbh + adv, idesc, accum);
+              mma_tf32_2sm_warp(d, dah + adv_a, dbl + adv, idesc, 1u);
+              mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv, idesc, 1u);
             } else {
-              mma_tf32_2sm(d, dah + adv_a, dbh + adv, idesc, accum);
+              mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv, idesc, accum);
             }
           }
-          mma_commit_2sm_mc(&empty[s], 0x3);
+          mma_commit_2sm_mc_warp(&empty[s], 0x3);
+          if (THREE_X) mma_commit_2sm_mc_warp(&lo_empty[l], 0x3);
         }
-        mma_commit_2sm_mc(&tmem_full[acc], 0x3);
+        mma_commit_2sm_mc_warp(&tmem_full[acc], 0x3);
       }
     }
     __syncwarp();
@@ -294,8 +302,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       const int s = jt % S;
       mbar_wait(&ld_full[s], (jt / S) & 1);
       if (THREE_X) {
+        const int l = jt % SL;
+        const uint32_t ul = jt / SL;
+        if (ul > 0) mbar_wait(&lo_empty[l], (ul - 1) & 1);  // the MMA has finished reading this lo slot
         const uint32_t ah = smem_u32(a_hi(s));
-        const uint32_t al = smem_u32(a_lo(s));
+        const uint32_t al = smem_u32(a_lo(l));
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const uint32_t off = AMODE == A_NARROW ? (uint32_t)(t * 16 + i * 2048) : sw128_offset(rb + 16 * i, j);
@@ -364,6 +375,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     if (AMODE == A_GATHER) {
       cp_async_wait<0>();
       for (uint32_t jt = (it > (uint32_t)LAG ? it - LAG : 0); jt < it; ++jt) finalize(jt);
+    }
+    if (THREE_X) {  // drain: every lo slot released before exit (multicast commits target this CTA)
+      for (int i = 0; i < SL; ++i, ++it) {
+        const uint32_t ul = it / SL;
+        if (ul > 0) mbar_wait(&lo_empty[it % SL], (ul - 1) & 1);
+      }
     }
   } else {
     // ============================ epilogue (warps 6-9) ============================
@@ -559,6 +576,22 @@ cudaError_t launch_bn(int bn, const CUtensorMap& a, const CUtensorMap& bh, const
 }
 
 }  // namespace
+
+bool gemm2_encode_tiled(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
+                        const uint32_t* box, bool swizzle128) {
+  if (load_driver_fns() != cudaSuccess) return false;
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    es[i] = 1;
+    if (i < rank - 1) st[i] = strides[i];
+  }
+  return g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), d, st, b, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 int gemm2_choose_block_n(int64_t N) {
   if (N <= 64) return 64;

@@ -1,10 +1,12 @@
 // gemm2sm.h -- host interface of the persistent 2-CTA tcgen05 GEMM core (gemm2sm.cu).
 #pragma once
+#include <cuda.h>
+
 #include "internal.h"
 
 namespace conv2d {
 
-enum { A_IM2COL = 0, A_DENSE = 1, A_GATHER = 2, A_NARROW = 3, A_ROWSEG = 4 };
+enum { A_IM2COL = 0, A_DENSE = 1, A_GATHER = 2, A_NARROW = 3, A_ROWSEG = 4, A_HALO = 5 };
 
 struct Gemm2Args {
   int a_mode;              // A_IM2COL: a = NHWC input (C % 32 == 0), k = (r, s, c-block of 32)
@@ -34,6 +36,14 @@ struct Gemm2Args {
 };
 
 cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s);
+// rank-2..5 fp32 tiled tensor map (strides in bytes for dims 1..rank-1), L2 promotion 256 B, OOB -> 0
+bool gemm2_encode_tiled(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
+                        const uint32_t* box, bool swizzle128);
+
+// gemm_halo.cu: 3x3 stride-1 convolution with C % 32 == 0 as a halo-tile implicit GEMM (see file header)
+bool halo_ok(const Problem& p);
+cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_hi, const float* bt_lo, int64_t kpad,
+                             int64_t npad, int block_n, float* out, cudaStream_t s);
 int gemm2_choose_block_n(int64_t N);
 int gemm2_choose_splits(int64_t M, int64_t N, int nkb, int batch, int block_n);
 bool gemm2_im2col_ok(const Problem& p);

@@ -39,6 +39,9 @@ Plan make_plan(const Problem& p, bool is_1x1) {
   if (is_1x1 && p.C % 4 == 0 && p.C >= 32) {
     pl.a_mode = A_DENSE;
     pl.cstride = p.C;
+  } else if (!is_1x1 && halo_ok(p) && getenv("CONV2D_NO_HALO") == nullptr) {
+    pl.a_mode = A_HALO;  // 3x3 s1, small N: halo-tile reuse (gemm_halo.cu)
+    pl.cstride = p.C;
   } else if (gemm2_im2col_ok(p)) {
     pl.a_mode = A_IM2COL;
     pl.cstride = p.C;  // C % 32 == 0: one tap = C/32 whole k-blocks
@@ -62,8 +65,17 @@ Plan make_plan(const Problem& p, bool is_1x1) {
     pl.cstride = pl.cg;
   }
   if (pl.a_mode != A_ROWSEG) pl.rowstride = p.KW * pl.cstride;
+  if (const char* f = getenv("CONV2D_FORCE_AMODE")) {  // experiments: force the A-operand path
+    const int m = atoi(f);
+    if (m == A_GATHER) {
+      pl.a_mode = A_GATHER;
+      pl.cg = (int)round_up(p.C, 4);
+      pl.pad = pl.cg != p.C;
+      pl.cstride = pl.cg;
+    }
+  }
   pl.kpad = pl.a_mode == A_ROWSEG ? (int64_t)p.KH * 32 : round_up((int64_t)p.KH * p.KW * pl.cstride, 32);
-  pl.splits = (p.F % 4 == 0 && pl.a_mode != A_ROWSEG)
+  pl.splits = (p.F % 4 == 0 && pl.a_mode != A_ROWSEG && pl.a_mode != A_HALO)
                   ? gemm2_choose_splits(p.M(), p.F, (int)(pl.kpad / 32), 1, pl.block_n) : 1;
   pl.bt_bytes = round_up((int64_t)pl.npad * pl.kpad * 4, 256);
   pl.pad_bytes = !pl.pad ? 0
@@ -112,6 +124,7 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
   cudaError_t e =
       launch_filter_prep2(filt, p.KH, p.KW, p.C, p.F, pl.cstride, pl.rowstride, pl.kpad, pl.npad, bt_hi, bt_lo, s);
   if (e != cudaSuccess) return e;
+  if (pl.a_mode == A_HALO) return launch_gemm_halo(p, in, bt_hi, bt_lo, pl.kpad, pl.npad, pl.block_n, out, s);
   Gemm2Args g{};
   g.a_mode = pl.a_mode;
   g.a = in;

@@ -348,3 +348,52 @@ __device__ __forceinline__ void tma_store_4d(const void* tmap, uint32_t src, int
                : "memory");
 }
 }  // namespace sm100
+
+namespace sm100 {
+// SWIZZLE_128B K-major tile whose 8-row groups are `sbo` bytes apart and whose start row sits
+// `phase` rows into the 1024-byte swizzle period (matrix base offset, bits [49,52)).
+__device__ __forceinline__ uint64_t umma_desc_sw128_kmajor_sbo(uint32_t smem_addr, uint32_t sbo, uint32_t phase) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)(phase & 7u) << 49;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+__device__ __forceinline__ void tma_load_4d(const void* tmap, uint64_t* bar, uint32_t dst, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+}  // namespace sm100
+
+namespace sm100 {
+// Warp-collective variants: call with the WHOLE warp converged and warp-uniform operands; one
+// elected lane issues.  Keeping the warp converged lets ptxas hold descriptors in uniform
+// registers -- with a `lane == 0` guard it wraps every UTCHMMA in an ELECT/R2UR waterfall loop
+// (~10 extra instructions per MMA, which bounds N=64 tiles; profiles/round1_ncu.md).
+__device__ __forceinline__ void mma_tf32_2sm_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_2sm_mc_warp(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+}  // namespace sm100
