@@ -111,6 +111,15 @@ EDGE = [
     (1, 20, 20, 96, 257, 1, 1, 1, 1, 0),     # F = 257 (one past a tile)
     (2, 17, 19, 36, 24, 2, 4, 3, 2, 0),      # non-square window / stride
     (1, 130, 3, 8, 8, 3, 3, 1, 1, 0),        # M just over one 128-row tile per image row sweep
+    # halo-tile path (3x3 s1, C % 32 == 0, F <= 128): odd CTA-tile count, ragged spatial tiles
+    (1, 9, 13, 64, 40, 3, 3, 1, 1, 0),       # 2x2 CTA tiles -> 2 pairs, F%4==0 but < BN
+    (3, 17, 7, 96, 128, 3, 3, 1, 1, 1),      # VALID, 3 channel blocks, 15x5 output
+    (1, 16, 8, 32, 64, 3, 3, 1, 1, 0),       # exactly one CTA tile -> one real + one dummy tile
+    (2, 30, 31, 32, 66, 3, 3, 1, 1, 0),      # F=66 (F%4 != 0): direct-store epilogue
+    # row-segment stem path (C < 32, KW*C4 <= 32): C=3/5/8, strides, VALID
+    (2, 23, 19, 3, 64, 7, 7, 2, 2, 0),
+    (1, 20, 21, 5, 24, 3, 3, 1, 2, 1),
+    (3, 11, 12, 8, 16, 4, 4, 2, 1, 0),
 ]
 
 
