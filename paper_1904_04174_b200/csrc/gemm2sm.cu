@@ -51,6 +51,7 @@ struct DevArgs {
   int64_t M, N;
   int nkb, mt, nt, splits, batch, total_tiles;
   int wblk, hblk;  // A_ROWSEG: 16-wide / 16-high spatial pair-tile grid
+  int a_row_bytes; // A_ROWSEG: bytes TMA writes per 128-B smem row (KW*C4*4); the rest stays zero
   float* d;
   int64_t ldd, d_bstride;
   float* partial;
@@ -60,15 +61,19 @@ struct DevArgs {
 template <int BN, bool THREE_X>
 struct Cfg {
   static constexpr int BHALF = (BN / 2) * BK * 4;
-  // TMA ring stage: [A (raw fp32 = TF32 hi) | B_hi | B_lo (3xTF32)]; in 3xTF32 the A lo halves live in a
-  // separate, shallower ring so the TMA ring can run deeper (latency hiding for small-N tiles).
+  // TMA ring stage: [A (raw fp32 = TF32 hi) | B_hi | B_lo (3xTF32)].  3xTF32 keeps A's lo halves in
+  // TMEM (LO_TMEM: 32 columns per stage next to the two accumulators; the lo*hi MMA takes A from
+  // TMEM) when 2*BN leaves room, else in a separate smem ring (BN = 256).
+  static constexpr bool LO_TMEM = THREE_X && BN <= 128;
   static constexpr int STAGE = A_TILE + (THREE_X ? 2 : 1) * BHALF;
-  static constexpr int SL = THREE_X ? (BN == 128 ? 2 : 3) : 0;
+  static constexpr int SL = (THREE_X && !LO_TMEM) ? 3 : 0;
   static constexpr int EPI = 4 * 2 * 32 * 128;  // 4 epilogue warps x 2 buffers x (32 rows x 128 B)
   static constexpr int BUDGET = 232448 - EPI - 1024 - 512 - SL * A_TILE;
-  static constexpr int STAGES = (BUDGET / STAGE) > 12 ? 12 : (BUDGET / STAGE);
+  static constexpr int SMAX = LO_TMEM ? (512 - 2 * BN) / 32 : 12;
+  static constexpr int STAGES = (BUDGET / STAGE) > SMAX ? SMAX : (BUDGET / STAGE);
   static constexpr int SMEM = STAGES * STAGE + SL * A_TILE + EPI + 1024 + 512;
-  static constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulators
+  static constexpr uint32_t TMEM_COLS = LO_TMEM ? 512 : 2 * BN;
+  static constexpr uint32_t LO_COL0 = 2 * BN;  // first TMEM column of the lo slots (LO_TMEM)
 };
 
 struct Tile {
@@ -141,6 +146,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     tma_prefetch(&tmBh);
     if (THREE_X) tma_prefetch(&tmBl);
   }
+  if (AMODE == A_ROWSEG && args.a_row_bytes < 128) {
+    // TMA writes only the first a_row_bytes of each 128-byte row; the tail must read as 0.0 for the
+    // (zero-weight) padding k's, so clear every A stage once before any TMA traffic.
+    for (int i = threadIdx.x; i < S * (A_TILE / 16); i += NTHREADS)
+      sts128(smem_u32(a_hi(i / (A_TILE / 16))) + (uint32_t)(i % (A_TILE / 16)) * 16u, make_float4(0.f, 0.f, 0.f, 0.f));
+    fence_proxy_async_smem();
+  }
   if (warp == 5) tmem_alloc_2sm<C_::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   cluster_sync();
@@ -187,7 +199,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
       };
       uint32_t it = 0;
-      const uint32_t bytes = (AMODE != A_GATHER ? A_TILE : 0) + (THREE_X ? 2 : 1) * C_::BHALF;
+      // A_ROWSEG boxes are exactly KW*C4 floats wide (no OOB elements -> TMA fast path): fewer bytes
+      const uint32_t a_bytes = AMODE == A_GATHER ? 0u : AMODE == A_ROWSEG ? (uint32_t)args.a_row_bytes * 128u : A_TILE;
+      const uint32_t bytes = a_bytes + (THREE_X ? 2 : 1) * C_::BHALF;
       for (int t = cid; t < args.total_tiles; t += ncl) {
         const Tile tl = decode(args, t);
         const int64_t m_cta = (int64_t)tl.mi * 2 * BMC + rank * BMC;
@@ -265,8 +279,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const uint64_t dah = AMODE == A_NARROW ? umma_desc_interleave_kmajor(smem_u32(a_hi(s)), 2048, 128)
                                                  : umma_desc_sw128_kmajor(smem_u32(a_hi(s)));
           const uint64_t dbh = umma_desc_sw128_kmajor(smem_u32(b_hi(s)));
-          const int l = THREE_X ? (int)(it % SL) : 0;
-          const uint64_t dal = !THREE_X ? 0
+          const int l = (THREE_X && !C_::LO_TMEM) ? (int)(it % SL) : 0;
+          const uint32_t lo_t = tmem_base + C_::LO_COL0 + (uint32_t)(s * BK);  // LO_TMEM: stage s's lo columns
+          const uint64_t dal = (!THREE_X || C_::LO_TMEM) ? 0
                                : AMODE == A_NARROW ? umma_desc_interleave_kmajor(smem_u32(a_lo(l)), 2048, 128)
                                                    : umma_desc_sw128_kmajor(smem_u32(a_lo(l)));
           const uint64_t dbl = THREE_X ? umma_desc_sw128_kmajor(smem_u32(b_lo(s))) : 0;
@@ -276,7 +291,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             // narrow A: one K=8 step = two 16-byte core-matrix columns = 2 boxes = 4 KB
             const uint64_t adv_a = AMODE == A_NARROW ? (uint64_t)((k * 4096) >> 4) : adv;
             const uint32_t accum = (kb > tl.kb0 || k > 0) ? 1u : 0u;
-            if (THREE_X) {
+            if (THREE_X && C_::LO_TMEM) {
+              mma_tf32_2sm_ts_warp(d, lo_t + (uint32_t)(k * 8), dbh + adv, idesc, accum);
+              mma_tf32_2sm_warp(d, dah + adv_a, dbl + adv, idesc, 1u);
+              mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv, idesc, 1u);
+            } else if (THREE_X) {
               mma_tf32_2sm_warp(d, dal + adv_a, dbh + adv, idesc, accum);
               mma_tf32_2sm_warp(d, dah + adv_a, dbl + adv, idesc, 1u);
               mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv, idesc, 1u);
@@ -285,7 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             }
           }
           mma_commit_2sm_mc_warp(&empty[s], 0x3);
-          if (THREE_X) mma_commit_2sm_mc_warp(&lo_empty[l], 0x3);
+          if (THREE_X && !C_::LO_TMEM) mma_commit_2sm_mc_warp(&lo_empty[l], 0x3);
         }
         mma_commit_2sm_mc_warp(&tmem_full[acc], 0x3);
       }
@@ -301,7 +320,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     auto finalize = [&](uint32_t jt) {
       const int s = jt % S;
       mbar_wait(&ld_full[s], (jt / S) & 1);
-      if (THREE_X) {
+      if (THREE_X && C_::LO_TMEM) {
+        // thread t owns A row t: read its 32 k's, write lo = x - trunc_tf32(x) to TMEM lane t, stage s's
+        // 32 lo columns (the lo*hi MMA reads A from there).  hi stays in smem as raw fp32.
+        const uint32_t ah = smem_u32(a_hi(s));
+        float lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t off = AMODE == A_NARROW ? (uint32_t)(c * 2048 + t * 16) : sw128_offset(t, c);
+          const float4 v = lds128(ah + off);
+          lo[4 * c] = v.x - tf32_hi(v.x);
+          lo[4 * c + 1] = v.y - tf32_hi(v.y);
+          lo[4 * c + 2] = v.z - tf32_hi(v.z);
+          lo[4 * c + 3] = v.w - tf32_hi(v.w);
+        }
+        tmem_st32(tmem_base + ((uint32_t)(warp * 32) << 16) + C_::LO_COL0 + (uint32_t)(s * BK), lo);
+        tmem_st_wait();
+        tc_fence_before();
+      } else if (THREE_X) {
         const int l = jt % SL;
         const uint32_t ul = jt / SL;
         if (ul > 0) mbar_wait(&lo_empty[l], (ul - 1) & 1);  // the MMA has finished reading this lo slot
@@ -376,7 +412,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       cp_async_wait<0>();
       for (uint32_t jt = (it > (uint32_t)LAG ? it - LAG : 0); jt < it; ++jt) finalize(jt);
     }
-    if (THREE_X) {  // drain: every lo slot released before exit (multicast commits target this CTA)
+    if (THREE_X && !C_::LO_TMEM) {  // drain: every lo slot released before exit (multicast commits target us)
       for (int i = 0; i < SL; ++i, ++it) {
         const uint32_t ul = it / SL;
         if (ul > 0) mbar_wait(&lo_empty[it % SL], (ul - 1) & 1);
@@ -542,7 +578,7 @@ bool make_rowseg(CUtensorMap* m, const Problem& p, const float* xp, int cg, int 
                         (cuuint64_t)p.KH};
   cuuint64_t strides[4] = {(cuuint64_t)p.SW * cg * 4, (cuuint64_t)p.SH * wp * cg * 4, (cuuint64_t)hp * wp * cg * 4,
                            (cuuint64_t)wp * cg * 4};
-  cuuint32_t box[5] = {32, 16, 8, 1, 1};
+  cuuint32_t box[5] = {(cuuint32_t)(p.KW * cg), 16, 8, 1, 1};  // exactly the segment: no OOB elements
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   return g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(xp), dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -647,6 +683,7 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   a.nkb = (int)(g.kpad / 32);
   a.mt = (int)((g.M + 255) / 256);
   if (g.a_mode == A_ROWSEG) {
+    a.a_row_bytes = p.KW * g.gather_c * 4;
     a.wblk = (p.WO + 15) / 16;
     a.hblk = (p.HO + 15) / 16;
     a.mt = p.N * a.wblk * a.hblk;
