@@ -197,22 +197,34 @@ conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int de
   for (int ai = 1; ai < CONV2D_NUM_ALGOS && st == CONV2D_OK; ++ai) {
     const conv2d_algo_t a = (conv2d_algo_t)ai;
     if (!algo_supports(q, a)) continue;
-    for (int w = 0; w < warm && st == CONV2D_OK; ++w) st = run_algo(q, a, in, filt, out, ws, s);
+    // algorithm parameters: time every variant of the algorithm, keep its best
+    const bool gemm_like = a == CONV2D_ALGO_IMPLICIT_GEMM || a == CONV2D_ALGO_MATMUL_1X1;
+    const bool is_1x1 = a == CONV2D_ALGO_MATMUL_1X1;
+    const int nvar = gemm_like ? igemm_num_variants(q, is_1x1) : 1;
     double t_best = 1e300;
-    for (int r = 0; r < reps && st == CONV2D_OK; ++r) {
-      cudaEventRecord(e0, s);
-      st = run_algo(q, a, in, filt, out, ws, s);
-      cudaEventRecord(e1, s);
-      ce = cudaEventSynchronize(e1);
-      if (ce != cudaSuccess) {
-        st = cuda_fail(ce, "autotune sync");
-        break;
+    int v_best = 0;
+    for (int v = 0; v < nvar && st == CONV2D_OK; ++v) {
+      if (gemm_like) igemm_set_variant(q, is_1x1, v);
+      for (int w = 0; w < warm && st == CONV2D_OK; ++w) st = run_algo(q, a, in, filt, out, ws, s);
+      for (int r = 0; r < reps && st == CONV2D_OK; ++r) {
+        cudaEventRecord(e0, s);
+        st = run_algo(q, a, in, filt, out, ws, s);
+        cudaEventRecord(e1, s);
+        ce = cudaEventSynchronize(e1);
+        if (ce != cudaSuccess) {
+          st = cuda_fail(ce, "autotune sync");
+          break;
+        }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < t_best) {
+          t_best = ms;
+          v_best = v;
+        }
       }
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, e0, e1);
-      if (ms < t_best) t_best = ms;
     }
     if (st != CONV2D_OK) break;
+    if (gemm_like) igemm_set_variant(q, is_1x1, v_best);
     g_tune_times[ai] = t_best * 1000.0;
     if (t_best < best_t) {  // strict: ties keep the earlier enum
       best_t = t_best;

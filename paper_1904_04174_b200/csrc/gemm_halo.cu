@@ -44,15 +44,23 @@ struct HArgs {
 template <int BN, bool THREE_X>
 struct HCfg {
   static constexpr int BHALF = (BN / 2) * BK * 4;
+  static constexpr int BFULL = BN * BK * 4;
   static constexpr int HS = THREE_X ? 2 : 3;                           // halo slots
   static constexpr int HSLOT = HALO_BYTES * (THREE_X ? 2 : 1);         // hi (+ lo)
-  static constexpr int BSTAGE = BHALF * (THREE_X ? 2 : 1);
+  // CONCAT (3xTF32, BN = 64, where smem operand reads bound the MMA): B stage Z = BN rows (CTA0:
+  // B_hi, CTA1: B_lo) for one N'=2BN MMA hi x [B_hi | B_lo] -- A_hi is read once for both products --
+  // plus X = BN/2 rows of B_hi (this CTA's half) for lo x B_hi; the epilogue adds the two column halves.
+  // Otherwise (BN = 128, TF32): X = B_hi half [+ B_lo half], three / one MMAs per K step.
+  static constexpr bool CONCAT = THREE_X && BN == 64;
+  static constexpr int BSTAGE = CONCAT ? BFULL + BHALF : (THREE_X ? 2 : 1) * BHALF;
+  static constexpr int ACC = CONCAT ? 2 * BN : BN;                     // TMEM columns per accumulator
   static constexpr int EPI = 4 * 2 * 32 * 128;
   static constexpr int BUDGET = 232448 - EPI - 1024 - 512 - HS * HSLOT;
   static constexpr int S = (BUDGET / BSTAGE) > 12 ? 12 : (BUDGET / BSTAGE);
   static constexpr int SMEM = HS * HSLOT + S * BSTAGE + EPI + 1024 + 512;
-  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr uint32_t TMEM_COLS = 2 * ACC;
   static_assert(S >= 2, "halo kernel needs >= 2 B stages");
+  static_assert(2 * ACC <= 512, "TMEM");
 };
 
 struct HTile {
@@ -72,7 +80,8 @@ __device__ __forceinline__ HTile hdecode(const HArgs& a, int t, uint32_t rank) {
 template <int BN, bool THREE_X>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmBh,
-                const __grid_constant__ CUtensorMap tmBl, const __grid_constant__ CUtensorMap tmD,
+                const __grid_constant__ CUtensorMap tmBhF, const __grid_constant__ CUtensorMap tmBlF,
+                const __grid_constant__ CUtensorMap tmD,
                 const __grid_constant__ HArgs args) {
   using C_ = HCfg<BN, THREE_X>;
   constexpr int HS = C_::HS, S = C_::S;
@@ -80,8 +89,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   auto halo_hi = [&](int h) { return smem + (size_t)h * C_::HSLOT; };
   auto halo_lo = [&](int h) { return smem + (size_t)h * C_::HSLOT + HALO_BYTES; };
-  auto b_hi = [&](int s) { return smem + (size_t)HS * C_::HSLOT + (size_t)s * C_::BSTAGE; };
-  auto b_lo = [&](int s) { return b_hi(s) + C_::BHALF; };
+  auto b_z = [&](int s) { return smem + (size_t)HS * C_::HSLOT + (size_t)s * C_::BSTAGE; };  // CONCAT only
+  auto b_x = [&](int s) { return b_z(s) + (C_::CONCAT ? C_::BFULL : 0); };                    // B_hi half
+  auto b_lo = [&](int s) { return b_x(s) + C_::BHALF; };                                      // 3x, !CONCAT
   uint8_t* epi_smem = smem + (size_t)HS * C_::HSLOT + (size_t)S * C_::BSTAGE;
   uint64_t* h_ld = reinterpret_cast<uint64_t*>(epi_smem + C_::EPI);
   uint64_t* h_full = h_ld + HS;
@@ -116,7 +126,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   if (warp == 4 && lane == 0) {
     tma_prefetch(&tmX);
     tma_prefetch(&tmBh);
-    if (THREE_X) tma_prefetch(&tmBl);
+    if (THREE_X) {
+      tma_prefetch(&tmBhF);
+      tma_prefetch(&tmBlF);  // !CONCAT: the B_lo half map
+    }
   }
   if (warp == 5) tmem_alloc_2sm<C_::TMEM_COLS>(tmem_slot);
   tc_fence_before();
@@ -143,8 +156,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             if (rank == 0) mbar_arrive_expect_tx(&b_full[s], 2 * C_::BSTAGE);
             const uint32_t fb = b_full_leader + (uint32_t)(s * sizeof(uint64_t));
             const int k0 = (tap * args.ncb + cb) * BK;  // filter prep order: k = tap * C + c
-            tma_load_3d_2sm(&tmBh, fb, smem_u32(b_hi(s)), k0, nrow, 0);
-            if (THREE_X) tma_load_3d_2sm(&tmBl, fb, smem_u32(b_lo(s)), k0, nrow, 0);
+            tma_load_3d_2sm(&tmBh, fb, smem_u32(b_x(s)), k0, nrow, 0);
+            if (C_::CONCAT)  // CTA0: B_hi rows [ni*BN, +BN); CTA1: B_lo rows [ni*BN, +BN)
+              tma_load_3d_2sm(rank == 0 ? (const void*)&tmBhF : (const void*)&tmBlF, fb, smem_u32(b_z(s)), k0,
+                              tl.ni * BN, 0);
+            else if (THREE_X)  // B_lo half (tmBlF holds the half-box B_lo map when !CONCAT)
+              tma_load_3d_2sm(&tmBlF, fb, smem_u32(b_lo(s)), k0, nrow, 0);
           }
         }
       }
@@ -157,12 +174,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     // ============================ MMA issuer (leader) ============================
     if (rank == 0) {  // whole warp, converged: operands stay warp-uniform
       constexpr uint32_t idesc = idesc_tf32(256, BN);
+      constexpr uint32_t idesc2 = idesc_tf32(256, 2 * BN);  // 3x: hi x [B_hi | B_lo]
       uint32_t hit = 0, bit = 0, ai = 0;
       for (int t = cid; t < args.total; t += ncl, ++ai) {
         const int acc = ai & 1;
         if (ai >= 2) mbar_wait(&tmem_empty[acc], ((ai >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+        const uint32_t d = tmem_base + (uint32_t)(acc * C_::ACC);
         for (int cb = 0; cb < args.ncb; ++cb, ++hit) {
           const int h = hit % HS;
           mbar_wait(&h_full[h], (hit / HS) & 1);
@@ -179,18 +197,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             const uint64_t dah = umma_desc_sw128_kmajor_sbo(smem_u32(halo_hi(h)) + off, HWD * 128, 0u);
             const uint64_t dal =
                 THREE_X ? umma_desc_sw128_kmajor_sbo(smem_u32(halo_lo(h)) + off, HWD * 128, 0u) : 0;
-            const uint64_t dbh = umma_desc_sw128_kmajor(smem_u32(b_hi(s)));
-            const uint64_t dbl = THREE_X ? umma_desc_sw128_kmajor(smem_u32(b_lo(s))) : 0;
+            const uint64_t dbx = umma_desc_sw128_kmajor(smem_u32(b_x(s)));
+            const uint64_t dbz = C_::CONCAT ? umma_desc_sw128_kmajor(smem_u32(b_z(s))) : 0;
+            const uint64_t dbl = (THREE_X && !C_::CONCAT) ? umma_desc_sw128_kmajor(smem_u32(b_lo(s))) : 0;
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
               const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);
               const uint32_t accum = (cb > 0 || tap > 0 || k > 0) ? 1u : 0u;
-              if (THREE_X) {
-                mma_tf32_2sm_warp(d, dal + adv, dbh + adv, idesc, accum);
+              if (THREE_X && !C_::CONCAT) {
+                mma_tf32_2sm_warp(d, dal + adv, dbx + adv, idesc, accum);
                 mma_tf32_2sm_warp(d, dah + adv, dbl + adv, idesc, 1u);
-                mma_tf32_2sm_warp(d, dah + adv, dbh + adv, idesc, 1u);
+                mma_tf32_2sm_warp(d, dah + adv, dbx + adv, idesc, 1u);
+              } else if (C_::CONCAT) {
+                // cols [0,BN) += hi*B_hi, cols [BN,2BN) += hi*B_lo   (A_hi read once for both products)
+                mma_tf32_2sm_warp(d, dah + adv, dbz + adv, idesc2, accum);
+                // cols [0,BN) += lo*B_hi
+                mma_tf32_2sm_warp(d, dal + adv, dbx + adv, idesc, 1u);
               } else {
-                mma_tf32_2sm_warp(d, dah + adv, dbh + adv, idesc, accum);
+                mma_tf32_2sm_warp(d, dah + adv, dbx + adv, idesc, accum);
               }
             }
             mma_commit_2sm_mc_warp(&b_empty[s], 0x3);
@@ -243,7 +267,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C_::ACC + c0), v);
+        if (C_::CONCAT) {  // add the hi*B_lo correction columns
+          float w[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C_::ACC + BN + c0), w);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) v[k] += w[k];
+        }
         if (c0 + 32 >= BN) {
           tc_fence_before();
           mbar_arrive_remote(tmem_empty_leader + (uint32_t)(acc * sizeof(uint64_t)));
@@ -285,8 +315,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 }
 
 template <int BN, bool THREE_X>
-cudaError_t launch_h(const CUtensorMap& x, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& dm,
-                     const HArgs& a, int clusters, cudaStream_t s) {
+cudaError_t launch_h(const CUtensorMap& x, const CUtensorMap& bh, const CUtensorMap& bhf, const CUtensorMap& blf,
+                     const CUtensorMap& dm, const HArgs& a, int clusters, cudaStream_t s) {
   using C_ = HCfg<BN, THREE_X>;
   auto kern = halo_kernel<BN, THREE_X>;
   static bool attr = false;
@@ -295,7 +325,7 @@ cudaError_t launch_h(const CUtensorMap& x, const CUtensorMap& bh, const CUtensor
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<dim3(2 * clusters), NTHREADS, C_::SMEM, s>>>(x, bh, bl, dm, a);
+  kern<<<dim3(2 * clusters), NTHREADS, C_::SMEM, s>>>(x, bh, bhf, blf, dm, a);
   return cudaGetLastError();
 }
 
@@ -322,7 +352,7 @@ cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_
   a.F = p.F;
   a.ldd = p.F;
   a.d = out;
-  alignas(64) CUtensorMap tx{}, tbh{}, tbl{}, td{};
+  alignas(64) CUtensorMap tx{}, tbh{}, tbhf{}, tblf{}, td{};
   {  // input halo boxes: {32 ch, 16 w, 18 h, 1 n} over NHWC, OOB (padding) -> 0
     const uint64_t dims[4] = {(uint64_t)p.C, (uint64_t)p.W, (uint64_t)p.H, (uint64_t)p.N};
     const uint64_t st[3] = {(uint64_t)p.C * 4, (uint64_t)p.W * p.C * 4, (uint64_t)p.H * p.W * p.C * 4};
@@ -333,9 +363,17 @@ cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_
     const uint64_t dims[3] = {(uint64_t)kpad, (uint64_t)npad, 1};
     const uint64_t st[2] = {(uint64_t)kpad * 4, (uint64_t)kpad * 4 * npad};
     const uint32_t box[3] = {32, (uint32_t)block_n / 2, 1};
+    const uint32_t boxf[3] = {32, (uint32_t)block_n, 1};
     if (!gemm2_encode_tiled(&tbh, 3, bt_hi, dims, st, box, true)) return cudaErrorInvalidValue;
-    if (three_x && !gemm2_encode_tiled(&tbl, 3, bt_lo, dims, st, box, true)) return cudaErrorInvalidValue;
-    if (!three_x) tbl = tbh;
+    const bool concat = three_x && block_n == 64;
+    if (concat && (!gemm2_encode_tiled(&tbhf, 3, bt_hi, dims, st, boxf, true) ||
+                   !gemm2_encode_tiled(&tblf, 3, bt_lo, dims, st, boxf, true)))
+      return cudaErrorInvalidValue;
+    if (three_x && !concat) {  // half-box B_lo map in the tmBlF slot
+      if (!gemm2_encode_tiled(&tblf, 3, bt_lo, dims, st, box, true)) return cudaErrorInvalidValue;
+      tbhf = tbh;
+    }
+    if (!three_x) tbhf = tblf = tbh;
   }
   a.tma_store = 0;
   if (p.F % 4 == 0) {  // output boxes {32 f, 8 wo, 4 ho, 1 n}
@@ -347,10 +385,10 @@ cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_
   if (!a.tma_store) td = tbh;
   const int clusters = a.total < 74 ? a.total : 74;
   switch (block_n) {
-    case 64: return three_x ? launch_h<64, true>(tx, tbh, tbl, td, a, clusters, s)
-                            : launch_h<64, false>(tx, tbh, tbl, td, a, clusters, s);
-    case 128: return three_x ? launch_h<128, true>(tx, tbh, tbl, td, a, clusters, s)
-                             : launch_h<128, false>(tx, tbh, tbl, td, a, clusters, s);
+    case 64: return three_x ? launch_h<64, true>(tx, tbh, tbhf, tblf, td, a, clusters, s)
+                            : launch_h<64, false>(tx, tbh, tbhf, tblf, td, a, clusters, s);
+    case 128: return three_x ? launch_h<128, true>(tx, tbh, tbhf, tblf, td, a, clusters, s)
+                             : launch_h<128, false>(tx, tbh, tbhf, tblf, td, a, clusters, s);
   }
   return cudaErrorInvalidValue;
 }

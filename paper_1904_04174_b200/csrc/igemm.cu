@@ -13,6 +13,9 @@
 //   [split_reduce]  when the pair-tile count is below one wave
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "gemm2sm.h"
 
@@ -29,17 +32,35 @@ struct Plan {
   size_t bt_bytes, pad_bytes, partial_bytes, total;
 };
 
-Plan make_plan(const Problem& p, bool is_1x1) {
+// Per-layer algorithm parameters chosen by the auto-selector ("different parameters
+// for each algorithm"): bit 0 selects the alternative A-operand path (implicit_gemm: halo <-> im2col;
+// matmul_1x1: dense <-> im2col), bit 1 halves the N tile (256 -> 128: 3xTF32 lo halves then fit in
+// TMEM next to the accumulators, deeper TMA ring).
+using VKey = std::tuple<int, int, int, int, int, int, int, int, int, int, int, bool>;
+std::mutex g_vmu;
+std::map<VKey, int> g_variant;
+VKey vkey(const Problem& p, bool is_1x1) {
+  return VKey(p.N, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH, p.SW, p.pad_top * 64 + p.pad_left, (int)p.math, is_1x1);
+}
+int variant_of(const Problem& p, bool is_1x1) {
+  if (const char* f = getenv("CONV2D_FORCE_VARIANT")) return atoi(f) & 3;  // parity-test hook
+  std::lock_guard<std::mutex> lk(g_vmu);
+  auto it = g_variant.find(vkey(p, is_1x1));
+  return it == g_variant.end() ? 0 : it->second;
+}
+
+Plan make_plan(const Problem& p, bool is_1x1, int variant) {
   Plan pl{};
   pl.three_x = p.math == CONV2D_MATH_FP32;
   pl.block_n = gemm2_choose_block_n(p.F);
+  if ((variant & 2) && pl.block_n == 256) pl.block_n = 128;
   pl.npad = round_up(p.F, pl.block_n);
   pl.pad = false;
   pl.cg = p.C;
-  if (is_1x1 && p.C % 4 == 0 && p.C >= 32) {
+  if (is_1x1 && p.C % 4 == 0 && p.C >= 32 && !((variant & 1) && gemm2_im2col_ok(p))) {
     pl.a_mode = A_DENSE;
     pl.cstride = p.C;
-  } else if (!is_1x1 && halo_ok(p) && getenv("CONV2D_NO_HALO") == nullptr) {
+  } else if (!is_1x1 && halo_ok(p) && !(variant & 1) && getenv("CONV2D_NO_HALO") == nullptr) {
     pl.a_mode = A_HALO;  // 3x3 s1, small N: halo-tile reuse (gemm_halo.cu)
     pl.cstride = p.C;
   } else if (gemm2_im2col_ok(p)) {
@@ -87,16 +108,31 @@ Plan make_plan(const Problem& p, bool is_1x1) {
 }
 }  // namespace
 
-size_t igemm_workspace(const Problem& p, bool is_1x1) { return make_plan(p, is_1x1).total; }
+int igemm_num_variants(const Problem& p, bool is_1x1) {
+  const bool alt_a = is_1x1 ? (p.C % 4 == 0 && p.C >= 32 && gemm2_im2col_ok(p)) : (halo_ok(p) && gemm2_im2col_ok(p));
+  const bool alt_n = gemm2_choose_block_n(p.F) == 256;
+  return alt_n ? 4 : (alt_a ? 2 : 1);  // variants are bit masks: [A path][N tile]
+}
+
+void igemm_set_variant(const Problem& p, bool is_1x1, int v) {
+  std::lock_guard<std::mutex> lk(g_vmu);
+  g_variant[vkey(p, is_1x1)] = v;
+}
+
+size_t igemm_workspace(const Problem& p, bool is_1x1) {
+  size_t w = 0;
+  for (int v = 0; v < igemm_num_variants(p, is_1x1); ++v) w = std::max(w, make_plan(p, is_1x1, v).total);
+  return w;
+}
 
 int igemm_launches(const Problem& p, bool is_1x1) {
-  const Plan pl = make_plan(p, is_1x1);
+  const Plan pl = make_plan(p, is_1x1, variant_of(p, is_1x1));
   return 2 + (pl.pad ? 1 : 0) + (pl.splits > 1 ? 1 : 0);
 }
 
 cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const float* filt, float* out, void* ws,
                          cudaStream_t s) {
-  const Plan pl = make_plan(p, is_1x1);
+  const Plan pl = make_plan(p, is_1x1, variant_of(p, is_1x1));
   static const bool debug = getenv("CONV2D_DEBUG") != nullptr;
   if (debug)
     fprintf(stderr, "[conv2d] igemm N=%d H=%d W=%d C=%d F=%d K=%dx%d S=%d: a_mode=%d bn=%d splits=%d kpad=%lld 3x=%d\n",

@@ -214,3 +214,24 @@ def test_tf32_mma_reads_truncated_operands(cuda_ok):
     wt = (w.view(np.uint32) & np.uint32(0xFFFFE000)).view(np.float32)
     a = C().ALGO_IMPLICIT_GEMM
     assert np.array_equal(gpu_conv(p, x, w, a), gpu_conv(p, xt, wt, a))
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("case", [(2, 28, 28, 64, 64, 3, 3, 1, 1, 0), (1, 14, 15, 128, 128, 3, 3, 1, 1, 1),
+                                  (2, 12, 12, 64, 256, 1, 1, 1, 1, 0), (1, 9, 9, 64, 320, 3, 3, 2, 2, 0)], ids=str)
+def test_algorithm_parameter_variants(cuda_ok, monkeypatch, variant, case):
+    """Both A-operand variants the auto-selector may pick per layer (implicit_gemm: halo <-> im2col,
+    matmul_1x1: dense <-> im2col) give the same results (integer-exact and within tolerance)."""
+    monkeypatch.setenv("CONV2D_FORCE_VARIANT", str(variant))
+    p0 = P(*case)
+    x, w = make_inputs(p0, layer_id=900)
+    ref, den = O.conv2d(oparams(p0), x, w, with_denom=True)
+    xi, wi = make_inputs(p0, layer_id=901, dist=synth.DIST_INT5)
+    refi = O.conv2d(oparams(p0), xi, wi)
+    for math in MATHS:
+        p = p0.replace(math=math)
+        for a in (C().ALGO_IMPLICIT_GEMM, C().ALGO_MATMUL_1X1):
+            if not C().conv2d_supports(p, a):
+                continue
+            check_close(p, gpu_conv(p, x, w, a), ref, den, a, f"variant {variant} {case} {math} {a}")
+            assert np.array_equal(gpu_conv(p, xi, wi, a), refi)
