@@ -139,36 +139,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 
   if (warp == 4) {
     // ============================ TMA producer ============================
+    // Work is a flat sequence of "units" (tile, channel block); the halo of unit u+1 is issued
+    // before the nine B loads of unit u so it lands while unit u's MMAs run.
     if (lane == 0) {
       const uint32_t b_full_leader = mapa(smem_u32(b_full), 0);
-      uint32_t hit = 0, bit = 0;
-      for (int t = cid; t < args.total; t += ncl) {
-        const HTile tl = hdecode(args, t, rank);
+      const int my_tiles = args.total > cid ? (args.total - cid + ncl - 1) / ncl : 0;
+      const int units = my_tiles * args.ncb;
+      auto issue_halo = [&](int u) {
+        const HTile tl = hdecode(args, cid + (u / args.ncb) * ncl, rank);
+        const int cb = u % args.ncb;
+        const int h = u % HS;
+        if (u >= HS) mbar_wait(&h_empty[h], ((u / HS) - 1) & 1);
+        mbar_arrive_expect_tx(&h_ld[h], HALO_BYTES);
+        tma_load_4d(&tmX, &h_ld[h], smem_u32(halo_hi(h)), cb * BK, tl.wo0 - args.PL, tl.ho0 - args.PT, tl.n);
+      };
+      if (units > 0) issue_halo(0);
+      uint32_t bit = 0;
+      for (int u = 0; u < units; ++u) {
+        if (u + 1 < units) issue_halo(u + 1);
+        const HTile tl = hdecode(args, cid + (u / args.ncb) * ncl, rank);
+        const int cb = u % args.ncb;
         const int nrow = tl.ni * BN + (int)rank * (BN / 2);
-        for (int cb = 0; cb < args.ncb; ++cb, ++hit) {
-          const int h = hit % HS;
-          if (hit >= (uint32_t)HS) mbar_wait(&h_empty[h], ((hit / HS) - 1) & 1);
-          mbar_arrive_expect_tx(&h_ld[h], HALO_BYTES);
-          tma_load_4d(&tmX, &h_ld[h], smem_u32(halo_hi(h)), cb * BK, tl.wo0 - args.PL, tl.ho0 - args.PT, tl.n);
-          for (int tap = 0; tap < taps; ++tap, ++bit) {
-            const int s = bit % S;
-            if (bit >= (uint32_t)S) mbar_wait(&b_empty[s], ((bit / S) - 1) & 1);
-            if (rank == 0) mbar_arrive_expect_tx(&b_full[s], 2 * C_::BSTAGE);
-            const uint32_t fb = b_full_leader + (uint32_t)(s * sizeof(uint64_t));
-            const int k0 = (tap * args.ncb + cb) * BK;  // filter prep order: k = tap * C + c
-            tma_load_3d_2sm(&tmBh, fb, smem_u32(b_x(s)), k0, nrow, 0);
-            if (C_::CONCAT)  // CTA0: B_hi rows [ni*BN, +BN); CTA1: B_lo rows [ni*BN, +BN)
-              tma_load_3d_2sm(rank == 0 ? (const void*)&tmBhF : (const void*)&tmBlF, fb, smem_u32(b_z(s)), k0,
-                              tl.ni * BN, 0);
-            else if (THREE_X)  // B_lo half (tmBlF holds the half-box B_lo map when !CONCAT)
-              tma_load_3d_2sm(&tmBlF, fb, smem_u32(b_lo(s)), k0, nrow, 0);
-          }
+        for (int tap = 0; tap < taps; ++tap, ++bit) {
+          const int s = bit % S;
+          if (bit >= (uint32_t)S) mbar_wait(&b_empty[s], ((bit / S) - 1) & 1);
+          if (rank == 0) mbar_arrive_expect_tx(&b_full[s], 2 * C_::BSTAGE);
+          const uint32_t fb = b_full_leader + (uint32_t)(s * sizeof(uint64_t));
+          const int k0 = (tap * args.ncb + cb) * BK;  // filter prep order: k = tap * C + c
+          tma_load_3d_2sm(&tmBh, fb, smem_u32(b_x(s)), k0, nrow, 0);
+          if (C_::CONCAT)  // CTA0: B_hi rows [ni*BN, +BN); CTA1: B_lo rows [ni*BN, +BN)
+            tma_load_3d_2sm(rank == 0 ? (const void*)&tmBhF : (const void*)&tmBlF, fb, smem_u32(b_z(s)), k0,
+                            tl.ni * BN, 0);
+          else if (THREE_X)  // B_lo half (tmBlF holds the half-box B_lo map when !CONCAT)
+            tma_load_3d_2sm(&tmBlF, fb, smem_u32(b_lo(s)), k0, nrow, 0);
         }
       }
       for (int i = 0; i < S; ++i, ++bit)
         if (bit >= (uint32_t)S) mbar_wait(&b_empty[bit % S], ((bit / S) - 1) & 1);
-      for (int i = 0; i < HS; ++i, ++hit)
-        if (hit >= (uint32_t)HS) mbar_wait(&h_empty[hit % HS], ((hit / HS) - 1) & 1);
+      for (int i = 0; i < HS; ++i) {
+        const int u = units + i;
+        if (u >= HS) mbar_wait(&h_empty[u % HS], ((u / HS) - 1) & 1);
+      }
     }
   } else if (warp == 5) {
     // ============================ MMA issuer (leader) ============================
