@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm2sm.h"
@@ -52,28 +53,35 @@ struct DevArgs {
   int nkb, mt, nt, splits, batch, total_tiles;
   int wblk, hblk;  // A_ROWSEG: 16-wide / 16-high spatial pair-tile grid
   int a_row_bytes; // A_ROWSEG: bytes TMA writes per 128-B smem row (KW*C4*4); the rest stays zero
+  int halo_row_floats, halo_bytes;  // A_STEM: floats per halo row ((15*SW+KW)*C4), bytes per halo
   float* d;
   int64_t ldd, d_bstride;
   float* partial;
   int tma_store;  // 1: epilogue stages 32x32 chunks in smem and writes them with TMA stores
 };
 
-template <int BN, bool THREE_X>
+template <int BN, bool THREE_X, bool BRES = false, bool STEMH = false>
 struct Cfg {
   static constexpr int BHALF = (BN / 2) * BK * 4;
   // TMA ring stage: [A (raw fp32 = TF32 hi) | B_hi | B_lo (3xTF32)].  3xTF32 keeps A's lo halves in
   // TMEM (LO_TMEM: 32 columns per stage next to the two accumulators; the lo*hi MMA takes A from
   // TMEM) when 2*BN leaves room, else in a separate smem ring (BN = 256).
+  // BRES: the CTA's whole B half (all k-blocks, hi [+ lo]) is loaded once per kernel into a 64 KB
+  // resident region and stages carry only A -- for single-N-tile, short-K layers where per-k-block
+  // B traffic is a third of the TMA engine's work (the C=3 stems, 1x1 layers).
   static constexpr bool LO_TMEM = THREE_X && BN <= 128;
-  static constexpr int STAGE = A_TILE + (THREE_X ? 2 : 1) * BHALF;
+  static constexpr int STAGE = BRES ? A_TILE : A_TILE + (THREE_X ? 2 : 1) * BHALF;
+  static constexpr int RES = BRES ? 65536 : 0;
   static constexpr int SL = (THREE_X && !LO_TMEM) ? 3 : 0;
   static constexpr int EPI = 4 * 2 * 32 * 128;  // 4 epilogue warps x 2 buffers x (32 rows x 128 B)
-  static constexpr int BUDGET = 232448 - EPI - 1024 - 512 - SL * A_TILE;
+  static constexpr int HALO = STEMH ? 2 * 16384 : 0;  // A_STEM: two input-halo slots
+  static constexpr int BUDGET = 232448 - EPI - 1024 - 512 - SL * A_TILE - RES - HALO;
   static constexpr int SMAX = LO_TMEM ? (512 - 2 * BN) / 32 : 12;
   static constexpr int STAGES = (BUDGET / STAGE) > SMAX ? SMAX : (BUDGET / STAGE);
-  static constexpr int SMEM = STAGES * STAGE + SL * A_TILE + EPI + 1024 + 512;
+  static constexpr int SMEM = STAGES * STAGE + SL * A_TILE + RES + HALO + EPI + 1024 + 512;
   static constexpr uint32_t TMEM_COLS = LO_TMEM ? 512 : 2 * BN;
   static constexpr uint32_t LO_COL0 = 2 * BN;  // first TMEM column of the lo slots (LO_TMEM)
+  static constexpr int RES_KB_MAX = RES / ((THREE_X ? 2 : 1) * BHALF);  // k-blocks that fit resident
 };
 
 struct Tile {
@@ -93,18 +101,19 @@ __device__ __forceinline__ Tile decode(const DevArgs& a, int t) {
   return r;
 }
 
-template <int BN, bool THREE_X, int AMODE>
+template <int BN, bool THREE_X, int AMODE, bool BRES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     gemm2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
                    const __grid_constant__ CUtensorMap tmBl, const __grid_constant__ CUtensorMap tmD,
                    const __grid_constant__ DevArgs args) {
-  using C_ = Cfg<BN, THREE_X>;
+  using C_ = Cfg<BN, THREE_X, BRES, AMODE == A_STEM>;
   constexpr int S = C_::STAGES;
   constexpr int LAG = S - 1 < 6 ? S - 1 : 6;  // gather pipelining depth (cp.async groups in flight)
   static_assert(S >= 2, "need >= 2 stages");
   // RELAY: A passes through the transform warps (3xTF32 split or cp.async gather), which then
   // signal the leader; otherwise the TMA engines signal the leader's full barrier directly.
-  constexpr bool RELAY = THREE_X || AMODE == A_GATHER;
+  constexpr bool RELAY = THREE_X || AMODE == A_GATHER || AMODE == A_STEM;
+  constexpr bool SPATIAL = AMODE == A_ROWSEG || AMODE == A_STEM;  // 16x8 spatial CTA tiles
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -113,14 +122,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   auto b_hi = [&](int s) { return smem + (size_t)s * C_::STAGE + A_TILE; };
   auto b_lo = [&](int s) { return smem + (size_t)s * C_::STAGE + A_TILE + C_::BHALF; };
   auto a_lo = [&](int l) { return smem + (size_t)S * C_::STAGE + (size_t)l * A_TILE; };  // lo ring slot
-  uint8_t* epi_smem = smem + S * C_::STAGE + SL * A_TILE;  // 1024-aligned (all sizes multiples of 1024)
+  uint8_t* res = smem + S * C_::STAGE + SL * A_TILE;  // BRES: resident B, hi k-blocks then lo k-blocks
+  auto res_hi = [&](int kb) { return res + (size_t)kb * C_::BHALF; };
+  auto res_lo = [&](int kb) { return res + (size_t)(C_::RES / 2) + (size_t)kb * C_::BHALF; };
+  uint8_t* halo = res + C_::RES;  // A_STEM: two 16 KB input-halo slots
+  uint8_t* epi_smem = halo + C_::HALO;  // 1024-aligned (all sizes multiples of 1024)
   uint64_t* ld_full = reinterpret_cast<uint64_t*>(epi_smem + C_::EPI);
   uint64_t* full = ld_full + S;
   uint64_t* empty = full + S;
   uint64_t* lo_empty = empty + S;
   uint64_t* tmem_full = lo_empty + (SL > 0 ? SL : 1);
   uint64_t* tmem_empty = tmem_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* b_res = tmem_empty + 2;
+  uint64_t* hs_full = b_res + 1;    // A_STEM halo ring: TMA -> transform
+  uint64_t* hs_empty = hs_full + 2; //                   transform -> producer
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hs_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -139,6 +155,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       mbar_init(&tmem_full[a], 1);
       mbar_init(&tmem_empty[a], 2 * 128);
     }
+    mbar_init(b_res, 1);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&hs_full[h], 1);
+      mbar_init(&hs_empty[h], 128);
+    }
     fence_mbar_init();
   }
   if (warp == 4 && lane == 0) {
@@ -146,7 +167,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     tma_prefetch(&tmBh);
     if (THREE_X) tma_prefetch(&tmBl);
   }
-  if (AMODE == A_ROWSEG && args.a_row_bytes < 128) {
+  if ((AMODE == A_ROWSEG && args.a_row_bytes < 128) || AMODE == A_STEM) {
     // TMA writes only the first a_row_bytes of each 128-byte row; the tail must read as 0.0 for the
     // (zero-weight) padding k's, so clear every A stage once before any TMA traffic.
     for (int i = threadIdx.x; i < S * (A_TILE / 16); i += NTHREADS)
@@ -201,12 +222,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       uint32_t it = 0;
       // A_ROWSEG boxes are exactly KW*C4 floats wide (no OOB elements -> TMA fast path): fewer bytes
       const uint32_t a_bytes = AMODE == A_GATHER ? 0u : AMODE == A_ROWSEG ? (uint32_t)args.a_row_bytes * 128u : A_TILE;
-      const uint32_t bytes = a_bytes + (THREE_X ? 2 : 1) * C_::BHALF;
-      for (int t = cid; t < args.total_tiles; t += ncl) {
+      const uint32_t bytes = a_bytes + (BRES ? 0u : (uint32_t)((THREE_X ? 2 : 1) * C_::BHALF));
+      if (BRES) {  // whole B half of this CTA (single N tile: rows [rank*BN/2, +BN/2)), once, to the leader
+        const uint32_t rb = mapa(smem_u32(b_res), 0);
+        if (rank == 0) mbar_arrive_expect_tx(b_res, 2u * (uint32_t)(args.nkb * (THREE_X ? 2 : 1) * C_::BHALF));
+        for (int kb = 0; kb < args.nkb; ++kb) {
+          tma_load_3d_2sm(&tmBh, rb, smem_u32(res_hi(kb)), kb * BK, (int)rank * (BN / 2), 0);
+          if (THREE_X) tma_load_3d_2sm(&tmBl, rb, smem_u32(res_lo(kb)), kb * BK, (int)rank * (BN / 2), 0);
+        }
+      }
+      if (AMODE == A_STEM) {
+        uint32_t u = 0;
+        for (int t = cid; t < args.total_tiles; t += ncl, ++u) {
+          const Tile tl = decode(args, t);
+          const int wo0 = (tl.mi % args.wblk) * 16;
+          const int ho0 = ((tl.mi / args.wblk) % args.hblk) * 16 + (int)rank * 8;
+          const int h = u & 1;
+          if (u >= 2) mbar_wait(&hs_empty[h], ((u >> 1) - 1) & 1);
+          mbar_arrive_expect_tx(&hs_full[h], (uint32_t)args.halo_bytes);
+          tma_load_3d(&tmA, &hs_full[h], smem_u32(halo + h * 16384), wo0 * args.SW * args.Cg, ho0 * args.SH,
+                      tl.mi / (args.wblk * args.hblk));
+        }
+      }
+      for (int t = cid; t < args.total_tiles && AMODE != A_STEM; t += ncl) {
         const Tile tl = decode(args, t);
         const int64_t m_cta = (int64_t)tl.mi * 2 * BMC + rank * BMC;
         int wb = 0, hb = 0, nimg = 0;
-        if (AMODE == A_ROWSEG) {
+        if (SPATIAL) {
           wb = (tl.mi % args.wblk) * 16;
           hb = ((tl.mi / args.wblk) % args.hblk) * 16 + (int)rank * 8;
           nimg = tl.mi / (args.wblk * args.hblk);
@@ -235,8 +277,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               tma_load_5d(&tmA, &ld_full[s], smem_u32(a_hi(s)), 0, wb, hb, nimg, kb);
             else if (AMODE == A_DENSE)
               tma_load_3d(&tmA, &ld_full[s], smem_u32(a_hi(s)), kb * BK, (int)m_cta, tl.bz);
-            tma_load_3d(&tmBh, &ld_full[s], smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
-            if (THREE_X) tma_load_3d(&tmBl, &ld_full[s], smem_u32(b_lo(s)), kb * BK, nrow, tl.bz);
+            if (!BRES) {
+              tma_load_3d(&tmBh, &ld_full[s], smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
+              if (THREE_X) tma_load_3d(&tmBl, &ld_full[s], smem_u32(b_lo(s)), kb * BK, nrow, tl.bz);
+            }
           } else {
             // both CTAs' bytes land on the leader's full[s]; only the leader arms it
             if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes);
@@ -250,12 +294,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               tma_load_5d_2sm(&tmA, fb, smem_u32(a_hi(s)), 0, wb, hb, nimg, kb);
             else
               tma_load_3d_2sm(&tmA, fb, smem_u32(a_hi(s)), kb * BK, (int)m_cta, tl.bz);
-            tma_load_3d_2sm(&tmBh, fb, smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
+            if (!BRES) tma_load_3d_2sm(&tmBh, fb, smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
           }
         }
       }
-      // drain: every stage must be released before the CTA may exit (multicast commits target us)
-      for (int i = 0; i < S; ++i, ++it) {
+      // drain: every stage must be released before the CTA may exit (multicast commits target us);
+      // in A_STEM mode the transform warps own the stages and drain them
+      for (int i = 0; i < S && AMODE != A_STEM; ++i, ++it) {
         const uint32_t u = it / S;
         if (u > 0) mbar_wait(&empty[it % S], (u - 1) & 1);
       }
@@ -265,6 +310,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     if (rank == 0) {  // whole warp, converged: operands stay warp-uniform
       constexpr uint32_t idesc = idesc_tf32(2 * BMC, BN);
       uint32_t it = 0, ai = 0;
+      if (BRES) {
+        mbar_wait(b_res, 0);
+        tc_fence_after();
+      }
       for (int t = cid; t < args.total_tiles; t += ncl, ++ai) {
         const Tile tl = decode(args, t);
         const int acc = ai & 1;
@@ -278,13 +327,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           tc_fence_after();
           const uint64_t dah = AMODE == A_NARROW ? umma_desc_interleave_kmajor(smem_u32(a_hi(s)), 2048, 128)
                                                  : umma_desc_sw128_kmajor(smem_u32(a_hi(s)));
-          const uint64_t dbh = umma_desc_sw128_kmajor(smem_u32(b_hi(s)));
+          const uint64_t dbh = umma_desc_sw128_kmajor(smem_u32(BRES ? res_hi(kb) : b_hi(s)));
           const int l = (THREE_X && !C_::LO_TMEM) ? (int)(it % SL) : 0;
           const uint32_t lo_t = tmem_base + C_::LO_COL0 + (uint32_t)(s * BK);  // LO_TMEM: stage s's lo columns
           const uint64_t dal = (!THREE_X || C_::LO_TMEM) ? 0
                                : AMODE == A_NARROW ? umma_desc_interleave_kmajor(smem_u32(a_lo(l)), 2048, 128)
                                                    : umma_desc_sw128_kmajor(smem_u32(a_lo(l)));
-          const uint64_t dbl = THREE_X ? umma_desc_sw128_kmajor(smem_u32(b_lo(s))) : 0;
+          const uint64_t dbl = THREE_X ? umma_desc_sw128_kmajor(smem_u32(BRES ? res_lo(kb) : b_lo(s))) : 0;
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
             const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);
@@ -319,7 +368,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 
     auto finalize = [&](uint32_t jt) {
       const int s = jt % S;
-      mbar_wait(&ld_full[s], (jt / S) & 1);
+      if (AMODE != A_STEM) mbar_wait(&ld_full[s], (jt / S) & 1);
       if (THREE_X && C_::LO_TMEM) {
         // thread t owns A row t: read its 32 k's, write lo = x - trunc_tf32(x) to TMEM lane t, stage s's
         // 32 lo columns (the lo*hi MMA reads A from there).  hi stays in smem as raw fp32.
@@ -404,8 +453,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             finalize(it - LAG);
           }
         }
+      } else if (AMODE == A_STEM) {
+        // thread t builds A row t = (ho_l, wo_l) = (t / 16, t % 16) of this CTA's 16x8 tile: for kernel
+        // row r, the KW*C4 contiguous halo floats at halo row ho_l*SH + r, column wo_l*SW*C4; the
+        // remaining chunks of the 128-B row stay zero (cleared at kernel start).
+        const uint32_t uh = (uint32_t)((tt - cid) / ncl);
+        const int h = uh & 1;
+        mbar_wait(&hs_full[h], (uh >> 1) & 1);
+        const uint32_t hbase = smem_u32(halo + h * 16384) +
+                               (uint32_t)(((t / 16) * args.SH * args.halo_row_floats + (t % 16) * args.SW * args.Cg) * 4);
+        const int nchunk = args.a_row_bytes / 16;
+        for (int kb = tl.kb0; kb < tl.kb1; ++kb, ++it) {
+          const int s = it % S;
+          const uint32_t u = it / S;
+          if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+          const uint32_t src = hbase + (uint32_t)(kb * args.halo_row_floats * 4);
+          const uint32_t sa = smem_u32(a_hi(s));
+          float lo[32];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c < nchunk) {
+              v = lds128(src + c * 16);
+              sts128(sa + sw128_offset(t, c), v);
+            }
+            lo[4 * c] = v.x - tf32_hi(v.x);
+            lo[4 * c + 1] = v.y - tf32_hi(v.y);
+            lo[4 * c + 2] = v.z - tf32_hi(v.z);
+            lo[4 * c + 3] = v.w - tf32_hi(v.w);
+          }
+          if (THREE_X && C_::LO_TMEM) {  // lo straight from registers (no read-back)
+            tmem_st32(tmem_base + ((uint32_t)(warp * 32) << 16) + C_::LO_COL0 + (uint32_t)(s * BK), lo);
+            tmem_st_wait();
+            tc_fence_before();
+          }
+          fence_proxy_async_smem();
+          mbar_arrive_remote(full_leader + (uint32_t)(s * sizeof(uint64_t)));
+        }
+        mbar_arrive(&hs_empty[h]);
       } else if (RELAY) {
         for (int kb = tl.kb0; kb < tl.kb1; ++kb, ++it) finalize(it);
+      }
+    }
+    if (AMODE == A_STEM) {  // drain the stage ring (multicast commits from the MMA target this CTA)
+      for (int i = 0; i < S; ++i, ++it) {
+        const uint32_t u = it / S;
+        if (u > 0) mbar_wait(&empty[it % S], (u - 1) & 1);
       }
     }
     if (AMODE == A_GATHER) {
@@ -436,8 +529,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       tc_fence_after();
       int64_t row0 = (int64_t)tl.mi * 2 * BMC + rank * BMC + q * 32;
       int64_t m = row0 + lane;
-      int sw0 = 0, sh0 = 0, sn = 0;  // A_ROWSEG: this warp's 16 x 2 spatial block
-      if (AMODE == A_ROWSEG) {
+      int sw0 = 0, sh0 = 0, sn = 0;  // A_ROWSEG / A_STEM: this warp's 16 x 2 spatial block
+      if (SPATIAL) {
         sw0 = (tl.mi % args.wblk) * 16;
         sh0 = ((tl.mi / args.wblk) % args.hblk) * 16 + (int)rank * 8 + 2 * q;
         sn = tl.mi / (args.wblk * args.hblk);
@@ -468,7 +561,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              if (AMODE == A_ROWSEG) tma_store_4d(&tmD, buf, n0 + c0, sw0, sh0, sn);
+              if (SPATIAL) tma_store_4d(&tmD, buf, n0 + c0, sw0, sh0, sn);
               else tma_store_3d(&tmD, buf, n0 + c0, (int)row0, z);
               bulk_commit();
             }
@@ -585,11 +678,11 @@ bool make_rowseg(CUtensorMap* m, const Problem& p, const float* xp, int cg, int 
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool THREE_X, int AMODE>
+template <int BN, bool THREE_X, int AMODE, bool BRES>
 cudaError_t launch_t(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& dm,
                      const DevArgs& args, int clusters, cudaStream_t s) {
-  using C_ = Cfg<BN, THREE_X>;
-  auto kern = gemm2sm_kernel<BN, THREE_X, AMODE>;
+  using C_ = Cfg<BN, THREE_X, BRES, AMODE == A_STEM>;
+  auto kern = gemm2sm_kernel<BN, THREE_X, AMODE, BRES>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
@@ -603,10 +696,28 @@ cudaError_t launch_t(const CUtensorMap& a, const CUtensorMap& bh, const CUtensor
 template <bool THREE_X, int AMODE>
 cudaError_t launch_bn(int bn, const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl,
                       const CUtensorMap& dm, const DevArgs& args, int clusters, cudaStream_t s) {
+  // BRES: one N tile, no split-K / batching, and every k-block of this CTA's B half fits the region
+  const bool bres = AMODE == A_STEM ||
+                    (args.nt == 1 && args.splits == 1 && args.batch == 1 && getenv("CONV2D_NO_BRES") == nullptr &&
+                     (AMODE == A_ROWSEG || AMODE == A_DENSE || AMODE == A_IM2COL));
+  if (AMODE == A_STEM) {  // always B-resident; only instantiated where it fits (host checks gemm2_stem_ok)
+    if (bn == 64) return launch_t<64, THREE_X, AMODE, true>(a, bh, bl, dm, args, clusters, s);
+    if (bn == 128) return launch_t<128, THREE_X, AMODE, true>(a, bh, bl, dm, args, clusters, s);
+    return cudaErrorInvalidValue;
+  }
   switch (bn) {
-    case 64: return launch_t<64, THREE_X, AMODE>(a, bh, bl, dm, args, clusters, s);
-    case 128: return launch_t<128, THREE_X, AMODE>(a, bh, bl, dm, args, clusters, s);
-    case 256: return launch_t<256, THREE_X, AMODE>(a, bh, bl, dm, args, clusters, s);
+    case 64:
+      if (bres && args.nkb <= Cfg<64, THREE_X, true>::RES_KB_MAX)
+        return launch_t<64, THREE_X, AMODE, true>(a, bh, bl, dm, args, clusters, s);
+      return launch_t<64, THREE_X, AMODE, false>(a, bh, bl, dm, args, clusters, s);
+    case 128:
+      if (bres && args.nkb <= Cfg<128, THREE_X, true>::RES_KB_MAX)
+        return launch_t<128, THREE_X, AMODE, true>(a, bh, bl, dm, args, clusters, s);
+      return launch_t<128, THREE_X, AMODE, false>(a, bh, bl, dm, args, clusters, s);
+    case 256:
+      if (bres && args.nkb <= Cfg<256, THREE_X, true>::RES_KB_MAX)
+        return launch_t<256, THREE_X, AMODE, true>(a, bh, bl, dm, args, clusters, s);
+      return launch_t<256, THREE_X, AMODE, false>(a, bh, bl, dm, args, clusters, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -655,6 +766,16 @@ static bool corners_ok(const Problem& p) {
 
 bool gemm2_narrow_ok(const Problem& p) { return corners_ok(p); }
 
+bool gemm2_stem_ok(const Problem& p, int block_n, bool three_x) {
+  const int cg = (p.C + 3) / 4 * 4;
+  const int row_floats = (15 * p.SW + p.KW) * cg;
+  const int halo = (7 * p.SH + p.KH) * row_floats * 4;
+  const int res_kb = three_x ? Cfg<64, true, true, true>::RES_KB_MAX * 64 / block_n
+                             : Cfg<64, false, true, true>::RES_KB_MAX * 64 / block_n;
+  return gemm2_rowseg_ok(p) && p.F <= block_n && block_n <= 128 && row_floats <= 256 && halo <= 16384 &&
+         p.KH <= res_kb && p.SH <= 8;
+}
+
 bool gemm2_rowseg_ok(const Problem& p) {
   const int cg = (p.C + 3) / 4 * 4;
   return p.KW * cg <= 32 && p.C < 32 && p.KH <= 64;
@@ -682,8 +803,10 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   a.M = g.M; a.N = g.N;
   a.nkb = (int)(g.kpad / 32);
   a.mt = (int)((g.M + 255) / 256);
-  if (g.a_mode == A_ROWSEG) {
+  if (g.a_mode == A_ROWSEG || g.a_mode == A_STEM) {
     a.a_row_bytes = p.KW * g.gather_c * 4;
+    a.halo_row_floats = (15 * p.SW + p.KW) * g.gather_c;
+    a.halo_bytes = (7 * p.SH + p.KH) * a.halo_row_floats * 4;
     a.wblk = (p.WO + 15) / 16;
     a.hblk = (p.HO + 15) / 16;
     a.mt = p.N * a.wblk * a.hblk;
@@ -701,6 +824,12 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   if (g.a_mode == A_IM2COL) ok = make_im2col(&ta, p, g.a);
   else if (g.a_mode == A_NARROW) ok = make_im2col_narrow(&ta, p, g.gather_x, g.gather_c);
   else if (g.a_mode == A_ROWSEG) ok = make_rowseg(&ta, p, g.gather_x, g.gather_c, g.hp, g.wp);
+  else if (g.a_mode == A_STEM) {  // halo boxes over the padded input viewed as {Wp*C4 floats, Hp, N}
+    const uint64_t dims[3] = {(uint64_t)g.wp * g.gather_c, (uint64_t)g.hp, (uint64_t)p.N};
+    const uint64_t st[2] = {(uint64_t)g.wp * g.gather_c * 4, (uint64_t)g.hp * g.wp * g.gather_c * 4};
+    const uint32_t box[3] = {(uint32_t)a.halo_row_floats, (uint32_t)(7 * p.SH + p.KH), 1};
+    ok = gemm2_encode_tiled(&ta, 3, g.gather_x, dims, st, box, false);
+  }
   else if (g.a_mode == A_DENSE) ok = make_tiled_3d(&ta, g.a, g.a_k, g.M, g.batch, g.lda, BMC);
   ok = ok && make_tiled_3d(&tbh, g.bt_hi, g.kpad, g.npad, g.batch, g.kpad, g.block_n / 2);
   if (g.three_x) ok = ok && make_tiled_3d(&tbl, g.bt_lo, g.kpad, g.npad, g.batch, g.kpad, g.block_n / 2);
@@ -711,7 +840,7 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
     float* dbase = g.splits == 1 ? g.d : g.partial;
     const uint64_t planes = (uint64_t)g.batch * (g.splits == 1 ? 1 : g.splits);
     const bool dense_batch = g.splits > 1 || g.batch == 1 || g.d_batch_stride == g.M * g.ldd;
-    if (g.a_mode == A_ROWSEG) {
+    if (g.a_mode == A_ROWSEG || g.a_mode == A_STEM) {
       cuuint64_t dims[4] = {(cuuint64_t)g.N, (cuuint64_t)p.WO, (cuuint64_t)p.HO, (cuuint64_t)p.N};
       cuuint64_t strides[3] = {(cuuint64_t)g.ldd * 4, (cuuint64_t)g.ldd * 4 * p.WO,
                                (cuuint64_t)g.ldd * 4 * p.WO * p.HO};
@@ -742,6 +871,7 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
       case A_DENSE: e = launch_bn<true, A_DENSE>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
       case A_NARROW: e = launch_bn<true, A_NARROW>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
       case A_ROWSEG: e = launch_bn<true, A_ROWSEG>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
+      case A_STEM: e = launch_bn<true, A_STEM>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
       default: e = launch_bn<true, A_GATHER>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
     }
   } else {
@@ -750,6 +880,7 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
       case A_DENSE: e = launch_bn<false, A_DENSE>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
       case A_NARROW: e = launch_bn<false, A_NARROW>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
       case A_ROWSEG: e = launch_bn<false, A_ROWSEG>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
+      case A_STEM: e = launch_bn<false, A_STEM>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
       default: e = launch_bn<false, A_GATHER>(g.block_n, ta, tbh, tbl, td, a, clusters, s); break;
     }
   }

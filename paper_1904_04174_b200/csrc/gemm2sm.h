@@ -6,7 +6,7 @@
 
 namespace conv2d {
 
-enum { A_IM2COL = 0, A_DENSE = 1, A_GATHER = 2, A_NARROW = 3, A_ROWSEG = 4, A_HALO = 5 };
+enum { A_IM2COL = 0, A_DENSE = 1, A_GATHER = 2, A_NARROW = 3, A_ROWSEG = 4, A_HALO = 5, A_STEM = 6 };
 
 struct Gemm2Args {
   int a_mode;              // A_IM2COL: a = NHWC input (C % 32 == 0), k = (r, s, c-block of 32)
@@ -16,6 +16,9 @@ struct Gemm2Args {
                            //           k-block per kernel row r holds the KW*gather_c contiguous floats of
                            //           each output pixel (5-D tiled TMA over overlapping strides); the CTA
                            //           tile is a 16 (wo) x 8 (ho) spatial block, the pair tile 16 x 16
+                           // A_STEM  : same tiles and k order as A_ROWSEG, but TMA loads one compact input
+                           //           halo per tile and the transform warps assemble each kernel row's
+                           //           A tile from it (B resident); for the small-C stems
                            // A_DENSE : a = [batch][M][lda] K-major matrix, lda % 4 == 0
                            // A_GATHER: gather_x = NHWC input with gather_c (% 4 == 0) channels, flat k
   const float* a;
@@ -49,6 +52,7 @@ int gemm2_choose_splits(int64_t M, int64_t N, int nkb, int batch, int block_n);
 bool gemm2_im2col_ok(const Problem& p);
 bool gemm2_narrow_ok(const Problem& p);
 bool gemm2_rowseg_ok(const Problem& p);
+bool gemm2_stem_ok(const Problem& p, int block_n, bool three_x);
 
 // gemm_common.cu
 // Bt[n][tap*cstride + c] = w[tap][c][n] (HWCF viewed as taps x C x F) for c < C, n < F, tap < taps;

@@ -67,7 +67,9 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
     pl.a_mode = A_IM2COL;
     pl.cstride = p.C;  // C % 32 == 0: one tap = C/32 whole k-blocks
   } else if (gemm2_rowseg_ok(p)) {
-    pl.a_mode = A_ROWSEG;  // small C, narrow windows (the C=3 stems): one 128-B row per pixel per kernel row
+    // small C, narrow windows (the C=3 stems): A_ROWSEG (one overlapping-stride TMA box per kernel
+    // row) by default, A_STEM (halo + transform-built rows) as the tunable alternative
+    pl.a_mode = ((variant & 1) && gemm2_stem_ok(p, pl.block_n, pl.three_x)) ? A_STEM : A_ROWSEG;
     pl.cg = (int)round_up(p.C, 4);
     pl.pad = true;         // spatial + channel padding pass
     pl.cstride = pl.cg;
@@ -85,7 +87,6 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
     pl.pad = pl.cg != p.C;
     pl.cstride = pl.cg;
   }
-  if (pl.a_mode != A_ROWSEG) pl.rowstride = p.KW * pl.cstride;
   if (const char* f = getenv("CONV2D_FORCE_AMODE")) {  // experiments: force the A-operand path
     const int m = atoi(f);
     if (m == A_GATHER) {
@@ -95,12 +96,14 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
       pl.cstride = pl.cg;
     }
   }
-  pl.kpad = pl.a_mode == A_ROWSEG ? (int64_t)p.KH * 32 : round_up((int64_t)p.KH * p.KW * pl.cstride, 32);
-  pl.splits = (p.F % 4 == 0 && pl.a_mode != A_ROWSEG && pl.a_mode != A_HALO)
+  const bool rowk = pl.a_mode == A_ROWSEG || pl.a_mode == A_STEM;  // k = (kernel row, 32 floats)
+  if (!rowk) pl.rowstride = p.KW * pl.cstride;
+  pl.kpad = rowk ? (int64_t)p.KH * 32 : round_up((int64_t)p.KH * p.KW * pl.cstride, 32);
+  pl.splits = (p.F % 4 == 0 && !rowk && pl.a_mode != A_HALO)
                   ? gemm2_choose_splits(p.M(), p.F, (int)(pl.kpad / 32), 1, pl.block_n) : 1;
   pl.bt_bytes = round_up((int64_t)pl.npad * pl.kpad * 4, 256);
   pl.pad_bytes = !pl.pad ? 0
-                 : pl.a_mode == A_ROWSEG ? round_up((int64_t)p.N * pl.hp * pl.wp * pl.cg * 4, 256)
+                 : rowk ? round_up((int64_t)p.N * pl.hp * pl.wp * pl.cg * 4, 256)
                                          : round_up((int64_t)p.N * p.H * p.W * pl.cg * 4, 256);
   pl.partial_bytes = pl.splits > 1 ? (size_t)pl.splits * p.M() * p.F * 4 : 0;
   pl.total = pl.bt_bytes * (pl.three_x ? 2 : 1) + pl.pad_bytes + pl.partial_bytes;
@@ -109,7 +112,9 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
 }  // namespace
 
 int igemm_num_variants(const Problem& p, bool is_1x1) {
-  const bool alt_a = is_1x1 ? (p.C % 4 == 0 && p.C >= 32 && gemm2_im2col_ok(p)) : (halo_ok(p) && gemm2_im2col_ok(p));
+  const bool alt_a = is_1x1 ? (p.C % 4 == 0 && p.C >= 32 && gemm2_im2col_ok(p))
+                            : ((halo_ok(p) && gemm2_im2col_ok(p)) ||
+                               (gemm2_rowseg_ok(p) && gemm2_stem_ok(p, gemm2_choose_block_n(p.F), p.math == 0)));
   const bool alt_n = gemm2_choose_block_n(p.F) == 256;
   return alt_n ? 4 : (alt_a ? 2 : 1);  // variants are bit masks: [A path][N tile]
 }
@@ -150,7 +155,8 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
   if (pl.pad) {
     float* xp = reinterpret_cast<float*>(w8);
     w8 += pl.pad_bytes;
-    cudaError_t e = pl.a_mode == A_ROWSEG
+    const bool rowk = pl.a_mode == A_ROWSEG || pl.a_mode == A_STEM;
+    cudaError_t e = rowk
                         ? launch_pad_spatial(in, p.N, p.H, p.W, p.C, pl.hp, pl.wp, pl.cg, p.pad_top, p.pad_left, xp, s)
                         : launch_pad_channels(in, (int64_t)p.N * p.H * p.W, p.C, pl.cg, xp, s);
     if (e != cudaSuccess) return e;
