@@ -200,10 +200,12 @@ conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int de
     // algorithm parameters: time every variant of the algorithm, keep its best
     const bool gemm_like = a == CONV2D_ALGO_IMPLICIT_GEMM || a == CONV2D_ALGO_MATMUL_1X1;
     const bool is_1x1 = a == CONV2D_ALGO_MATMUL_1X1;
-    const int nvar = gemm_like ? igemm_num_variants(q, is_1x1) : 1;
+    int masks[8] = {0};
+    const int nvar = gemm_like ? igemm_variants(q, is_1x1, masks) : 1;
     double t_best = 1e300;
     int v_best = 0;
-    for (int v = 0; v < nvar && st == CONV2D_OK; ++v) {
+    for (int vi = 0; vi < nvar && st == CONV2D_OK; ++vi) {
+      const int v = masks[vi];
       if (gemm_like) igemm_set_variant(q, is_1x1, v);
       for (int w = 0; w < warm && st == CONV2D_OK; ++w) st = run_algo(q, a, in, filt, out, ws, s);
       for (int r = 0; r < reps && st == CONV2D_OK; ++r) {

@@ -520,7 +520,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const uint32_t tmem_empty_leader = mapa(smem_u32(tmem_empty), 0);
     const bool vec_ok = (args.ldd % 4) == 0;
     const uint32_t ebuf = smem_u32(epi_smem) + (uint32_t)(q * 2 * 4096);
-    if (args.tma_store && lane == 0) tma_prefetch(&tmD);
+    if (args.tma_store == 1 && lane == 0) tma_prefetch(&tmD);
     uint32_t ai = 0, chunk = 0;
     for (int t = cid; t < args.total_tiles; t += ncl, ++ai) {
       const Tile tl = decode(args, t);
@@ -550,7 +550,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           tc_fence_before();
           mbar_arrive_remote(tmem_empty_leader + (uint32_t)(acc * sizeof(uint64_t)));
         }
-        if (args.tma_store) {
+        if (args.tma_store == 2) {
+          // smem-staged coalesced stores through the LSU (keeps the TMA engine free for loads):
+          // STS the 32x32 chunk swizzled, then each lane stores 16 B of row (i/8), column group (i%8)
+          if (row0 < args.M && n0 + c0 < args.N) {
+            const uint32_t buf = ebuf;
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              sts128(buf + sw128_offset(lane, k), make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]));
+            __syncwarp();
+            const int cq = lane & 7;
+            const int64_t col = n0 + c0 + cq * 4;
+#pragma unroll
+            for (int r4 = 0; r4 < 32; r4 += 4) {
+              const int rr = r4 + (lane >> 3);
+              const float4 val = lds128(buf + sw128_offset(rr, cq));
+              int64_t mrow;
+              if (SPATIAL) {
+                const int ho = sh0 + rr / 16, wo = sw0 + rr % 16;
+                mrow = (ho < args.HO && wo < args.WO) ? ((int64_t)sn * args.HO + ho) * args.WO + wo : args.M;
+              } else {
+                mrow = row0 + rr;
+              }
+              if (mrow < args.M && col + 3 < args.N)
+                *reinterpret_cast<float4*>(D + mrow * args.ldd + col) = val;
+              else if (mrow < args.M)
+                for (int e = 0; e < 4; ++e)
+                  if (col + e < args.N) D[mrow * args.ldd + col + e] = (&val.x)[e];
+            }
+          }
+        } else if (args.tma_store) {
           if (row0 < args.M && n0 + c0 < args.N) {
             const uint32_t buf = ebuf + (chunk & 1) * 4096;
             if (lane == 0) bulk_wait_read<1>();  // the store issued two chunks ago has read `buf`
@@ -582,7 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
       }
     }
-    if (args.tma_store && lane == 0) bulk_wait<0>();
+    if (args.tma_store == 1 && lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();
@@ -860,7 +890,8 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
     }
   }
   if (!ok) return cudaErrorInvalidValue;
-  if (!a.tma_store) td = tbh;  // unused slot
+  if (g.epi_stg && a.tma_store && g.ldd % 4 == 0) a.tma_store = 2;  // tuned variant: LSU-staged stores
+  if (a.tma_store != 1) td = tbh;  // unused slot
   if (g.a_mode == A_GATHER) ta = tbh;  // unused operand slot
   if (!g.three_x) tbl = tbh;
 

@@ -36,6 +36,7 @@ struct Gemm2Args {
   int batch, splits, block_n;
   bool three_x;
   int hp, wp;              // A_ROWSEG: padded input extent
+  bool epi_stg;            // epilogue: smem-staged coalesced STG instead of TMA stores
 };
 
 cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s);

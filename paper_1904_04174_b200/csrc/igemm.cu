@@ -35,7 +35,8 @@ struct Plan {
 // Per-layer algorithm parameters chosen by the auto-selector ("different parameters
 // for each algorithm"): bit 0 selects the alternative A-operand path (implicit_gemm: halo <-> im2col;
 // matmul_1x1: dense <-> im2col), bit 1 halves the N tile (256 -> 128: 3xTF32 lo halves then fit in
-// TMEM next to the accumulators, deeper TMA ring).
+// TMEM next to the accumulators, deeper TMA ring), bit 2 stores the output through the LSU
+// (smem-staged coalesced STG) instead of TMA bulk stores (frees the TMA engine for loads).
 using VKey = std::tuple<int, int, int, int, int, int, int, int, int, int, int, bool>;
 std::mutex g_vmu;
 std::map<VKey, int> g_variant;
@@ -43,7 +44,7 @@ VKey vkey(const Problem& p, bool is_1x1) {
   return VKey(p.N, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH, p.SW, p.pad_top * 64 + p.pad_left, (int)p.math, is_1x1);
 }
 int variant_of(const Problem& p, bool is_1x1) {
-  if (const char* f = getenv("CONV2D_FORCE_VARIANT")) return atoi(f) & 3;  // parity-test hook
+  if (const char* f = getenv("CONV2D_FORCE_VARIANT")) return atoi(f) & 7;  // parity-test hook
   std::lock_guard<std::mutex> lk(g_vmu);
   auto it = g_variant.find(vkey(p, is_1x1));
   return it == g_variant.end() ? 0 : it->second;
@@ -111,12 +112,21 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
 }
 }  // namespace
 
-int igemm_num_variants(const Problem& p, bool is_1x1) {
+int igemm_variants(const Problem& p, bool is_1x1, int* masks) {
   const bool alt_a = is_1x1 ? (p.C % 4 == 0 && p.C >= 32 && gemm2_im2col_ok(p))
                             : ((halo_ok(p) && gemm2_im2col_ok(p)) ||
                                (gemm2_rowseg_ok(p) && gemm2_stem_ok(p, gemm2_choose_block_n(p.F), p.math == 0)));
   const bool alt_n = gemm2_choose_block_n(p.F) == 256;
-  return alt_n ? 4 : (alt_a ? 2 : 1);  // variants are bit masks: [A path][N tile]
+  int n = 0;
+  // bit 0: A path, bit 1: N tile.  Bit 2 (LSU-staged epilogue) is not enumerated: it measured slower
+  // than TMA stores on every paper layer (kept reachable through CONV2D_FORCE_VARIANT for experiments).
+  for (int m = 0; m < 4; ++m) {
+    if ((m & 1) && !alt_a) continue;
+    if ((m & 2) && !alt_n) continue;
+    if (masks) masks[n] = m;
+    ++n;
+  }
+  return n;
 }
 
 void igemm_set_variant(const Problem& p, bool is_1x1, int v) {
@@ -126,7 +136,9 @@ void igemm_set_variant(const Problem& p, bool is_1x1, int v) {
 
 size_t igemm_workspace(const Problem& p, bool is_1x1) {
   size_t w = 0;
-  for (int v = 0; v < igemm_num_variants(p, is_1x1); ++v) w = std::max(w, make_plan(p, is_1x1, v).total);
+  int masks[8];
+  const int n = igemm_variants(p, is_1x1, masks);
+  for (int i = 0; i < n; ++i) w = std::max(w, make_plan(p, is_1x1, masks[i]).total);
   return w;
 }
 
@@ -190,6 +202,7 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
   g.three_x = pl.three_x;
   g.hp = pl.hp;
   g.wp = pl.wp;
+  g.epi_stg = (variant_of(p, is_1x1) & 4) != 0;
   return launch_gemm2(p, g, s);
 }
 

@@ -30,7 +30,7 @@ cudaError_t launch_direct(const Problem& p, const float* in, const float* filt, 
 cudaError_t launch_tiled(const Problem& p, const float* in, const float* filt, float* out, cudaStream_t s);
 // ---- igemm.cu (implicit GEMM and 1x1 matmul on tcgen05)
 size_t igemm_workspace(const Problem& p, bool is_1x1);  // max over variants
-int igemm_num_variants(const Problem& p, bool is_1x1);   // algorithm-parameter variants the tuner may try
+int igemm_variants(const Problem& p, bool is_1x1, int* masks);  // tunable parameter masks (<= 8)
 void igemm_set_variant(const Problem& p, bool is_1x1, int v);
 int igemm_launches(const Problem& p, bool is_1x1);
 cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const float* filt, float* out, void* ws,
