@@ -181,11 +181,12 @@ def reference_arm(args):
 
 
 def workload_config(args, per_gpu):
-    return {"workload": "resnet50_v1.5_conv_stack (53 convs, BASELINE configs[4])", "global_batch": GLOBAL_BATCH,
+    gb = getattr(args, "global_batch", GLOBAL_BATCH)
+    return {"workload": "resnet50_v1.5_conv_stack (53 convs, BASELINE configs[4])", "global_batch": gb,
             "per_gpu_batch": per_gpu, "math": "3xtf32 (fp32-faithful)" if args.math == "fp32" else "tf32",
             "algo": "auto (measured per layer)", "parallelism": f"batch-shard x{args.gpus}",
             "l2": "flushed before every step (256 MiB write, outside the timed events); step working set ~22 GB",
-            "gflop_per_step": round(sum(l.flops(GLOBAL_BATCH) for _, l in L.resnet50_v15_stack()) / 1e9, 3)}
+            "gflop_per_step": round(sum(l.flops(gb) for _, l in L.resnet50_v15_stack()) / 1e9, 3)}
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -198,6 +199,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch eagerly instead of replaying CUDA graphs")
+    ap.add_argument("--global-batch", type=int, default=GLOBAL_BATCH,
+                    help="analysis only (default = BASELINE config 5's 256)")
     ap.add_argument("--layers-out", default="", help="write the per-layer table (JSON) here")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -217,7 +221,7 @@ def main():
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
     from paper_1904_04174_b200.shard import broadcast_choices, max_over_ranks, shard_range
-    img0, img1 = shard_range(GLOBAL_BATCH, world, rank)
+    img0, img1 = shard_range(args.global_batch, world, rank)
     B = img1 - img0
     math = C.MATH_FP32 if args.math == "fp32" else C.MATH_TF32
     stream = torch.cuda.current_stream()
@@ -277,6 +281,33 @@ def main():
     ev_step = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     ev_conv = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in convs]
                for _ in range(args.steps)]
+    # CUDA graphs: one captured graph per timed step (the 53 conv2d_forward launches + external timing
+    # events between them), replayed on the launching stream -- removes per-kernel launch gaps.
+    graphs = None
+    if not args.no_graph:
+        try:
+            cap = torch.cuda.Stream()
+            graphs = []
+            for k in range(args.steps):
+                ev_conv[k] = [(torch.cuda.Event(enable_timing=True, external=True),
+                               torch.cuda.Event(enable_timing=True, external=True)) for _ in convs]
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
+                    cs = torch.cuda.current_stream()
+                    for i, cv in enumerate(convs):
+                        ev_conv[k][i][0].record(cs)
+                        C.conv2d_forward(cv["p"], C.ALGO_AUTO, cv["x"], cv["w"], cv["y"], ws, ws.numel(), cs)
+                        ev_conv[k][i][1].record(cs)
+                graphs.append(g)
+            for g in graphs:  # warm replays
+                g.replay()
+            torch.cuda.synchronize()
+            ev_conv[0][0][0].elapsed_time(ev_conv[0][0][1])  # timing of external events works?
+        except Exception as exc:  # fall back to eager launches (reported in config)
+            print(f"[bench] CUDA graph capture unavailable ({exc!r}); timing eager launches", file=sys.stderr)
+            graphs = None
+            ev_conv = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                        for _ in convs] for _ in range(args.steps)]
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
@@ -288,7 +319,10 @@ def main():
     for k in range(args.steps):
         flush.zero_()
         ev_step[k][0].record(stream)
-        step(ev_conv[k])
+        if graphs is not None:
+            graphs[k].replay()
+        else:
+            step(ev_conv[k])
         ev_step[k][1].record(stream)
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
@@ -377,7 +411,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 3), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32" if math == C.MATH_FP32 else "tf32",
                 "data": "synthetic (seeded splitmix64 uniform[-1,1), device-generated)",
-                "config": workload_config(args, B), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "config": dict(workload_config(args, B), cuda_graph=graphs is not None),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "wall_s_timed": round(wall, 3),
                 "pct_of_peak": round(100 * value / 1e3 / (useful_peak * world), 2)}
         if args.layers_out:
