@@ -52,6 +52,7 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="time eager calls instead of CUDA-graph replays")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
 
@@ -95,13 +96,29 @@ def main():
                 C.conv2d_clear_selection_cache()
             for _ in range(args.warmup):
                 C.conv2d_forward(p, a, x, w, y, ws, ws.numel(), stream)
+            torch.cuda.synchronize()
+            # replay a captured CUDA graph of the call (as bench.py does) so host-side work -- tensor-map
+            # encoding, launch calls -- is not inside the device-timed interval
+            graph = None
+            if not args.eager:
+                try:
+                    graph = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+                        C.conv2d_forward(p, a, x, w, y, ws, ws.numel(), torch.cuda.current_stream())
+                    graph.replay()
+                    torch.cuda.synchronize()
+                except Exception:
+                    graph = None
             times = []
             for _ in range(args.iters):
                 if not args.no_flush:
                     flush.zero_()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                C.conv2d_forward(p, a, x, w, y, ws, ws.numel(), stream)
+                if graph is not None:
+                    graph.replay()
+                else:
+                    C.conv2d_forward(p, a, x, w, y, ws, ws.numel(), stream)
                 e1.record(stream)
                 e1.synchronize()
                 times.append(e0.elapsed_time(e1))
@@ -113,7 +130,8 @@ def main():
                 ent["chose"] = C.ALGO_NAMES[C.conv2d_selected(p)]
             row["algos"][name] = ent
         rows.append(row)
-        best_algo = min((k for k in row["algos"] if k != "auto"), key=lambda k: row["algos"][k]["best_us"])
+        cand = [k for k in row["algos"] if k != "auto"] or list(row["algos"])
+        best_algo = min(cand, key=lambda k: row["algos"][k]["best_us"])
         print(f"{l.name:4s} {str(row['tuple']):26s} roof {row['roofline_us']:9.1f}us  " +
               "  ".join(f"{k[:6]}:{v['gflops']/1e3:6.1f}TF({v['roofline_frac']:.2f})" for k, v in row["algos"].items())
               + f"  best={best_algo}", flush=True)

@@ -37,7 +37,8 @@ OK, ERR_INVALID_PARAMS, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_ALIGNMENT, ERR_NULL,
 EXPORTED = ["conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv2d_query_workspace",
             "conv2d_forward", "conv2d_autotune", "conv2d_selected", "conv2d_set_selected",
             "conv2d_clear_selection_cache", "conv2d_last_tune_times", "conv2d_launch_count",
-            "conv2d_synth_fill", "conv2d_status_string", "conv2d_algo_name", "conv2d_last_error"]
+            "conv2d_synth_fill", "conv2d_status_string", "conv2d_algo_name", "conv2d_last_error",
+            "conv2d_debug_trace"]
 
 
 class conv2d_params_t(ctypes.Structure):
@@ -74,6 +75,8 @@ _lib.conv2d_status_string.restype = ctypes.c_char_p
 _lib.conv2d_algo_name.argtypes = [ctypes.c_int]
 _lib.conv2d_algo_name.restype = ctypes.c_char_p
 _lib.conv2d_last_error.argtypes = []
+_lib.conv2d_debug_trace.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+_lib.conv2d_debug_trace.restype = ctypes.c_int
 _lib.conv2d_last_error.restype = ctypes.c_char_p
 for _f in ("conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv2d_query_workspace",
            "conv2d_forward", "conv2d_autotune", "conv2d_selected", "conv2d_set_selected",
@@ -205,6 +208,17 @@ def conv2d_status_string(s: int) -> str:
 
 def conv2d_last_error() -> str:
     return _lib.conv2d_last_error().decode()
+
+
+def conv2d_debug_trace(enable: int, read: bool = False) -> list:
+    """include/conv2d_debug.h: toggle the GEMM core's per-CTA globaltimer stamps; with read=True
+    returns the 148 x 8 stamps (ns) as a flat list."""
+    n = 148 * 8
+    buf = (ctypes.c_ulonglong * n)() if read else None
+    got = _lib.conv2d_debug_trace(int(enable), buf, n if read else 0)
+    if got < 0:
+        raise RuntimeError("conv2d_debug_trace failed")
+    return list(buf[:got]) if read else []
 
 
 # ------------------------------------------------------------------ convenience (torch in, torch out)

@@ -18,6 +18,7 @@
 #include <tuple>
 
 #include "internal.h"
+#include "../../include/conv2d_debug.h"
 
 using namespace conv2d;
 
@@ -200,7 +201,7 @@ conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int de
     // algorithm parameters: time every variant of the algorithm, keep its best
     const bool gemm_like = a == CONV2D_ALGO_IMPLICIT_GEMM || a == CONV2D_ALGO_MATMUL_1X1;
     const bool is_1x1 = a == CONV2D_ALGO_MATMUL_1X1;
-    int masks[8] = {0};
+    int masks[16] = {0};
     const int nvar = gemm_like ? igemm_variants(q, is_1x1, masks) : 1;
     double t_best = 1e300;
     int v_best = 0;
@@ -450,5 +451,9 @@ const char* conv2d_algo_name(conv2d_algo_t a) {
 }
 
 const char* conv2d_last_error(void) { return g_last_error.c_str(); }
+
+int conv2d_debug_trace(int enable, unsigned long long* host, int n) {
+  return conv2d::gemm2_trace(enable, host, n);
+}
 
 }  // extern "C"

@@ -58,7 +58,16 @@ struct DevArgs {
   int64_t ldd, d_bstride;
   float* partial;
   int tma_store;  // 1: epilogue stages 32x32 chunks in smem and writes them with TMA stores
+  int b_mn;  // 1: B read straight from the row-major K x F filter (MN-major operand; no filter_prep)
+  unsigned long long* trace;  // debug (conv2d_debug_trace): TRACE_SLOTS globaltimer stamps per CTA, or null
 };
+
+// debug trace slots (per CTA): entry, setup done, first TMA issued, first stage consumed by the MMA
+// (leader), first accumulator ready (epilogue), last epilogue store issued, stores drained, exit
+constexpr int TRACE_SLOTS = 8;
+__device__ __forceinline__ void trace_at(const DevArgs& a, int slot) {
+  if (a.trace) a.trace[blockIdx.x * TRACE_SLOTS + slot] = globaltimer_ns();
+}
 
 template <int BN, bool THREE_X, bool BRES = false, bool STEMH = false>
 struct Cfg {
@@ -136,13 +145,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   uint64_t* b_res = tmem_empty + 2;
   uint64_t* hs_full = b_res + 1;    // A_STEM halo ring: TMA -> transform
   uint64_t* hs_empty = hs_full + 2; //                   transform -> producer
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hs_empty + 2);
+  uint64_t* b_ready = hs_empty + 2; // BRES + b_mn + 3xTF32: both CTAs' resident lo halves written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_ready + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int cid = (int)cluster_id_x();
   const int ncl = (int)nclusters_x();
+  if (threadIdx.x == 0) trace_at(args, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -156,6 +167,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       mbar_init(&tmem_empty[a], 2 * 128);
     }
     mbar_init(b_res, 1);
+    mbar_init(b_ready, 2 * 128);
     for (int h = 0; h < 2; ++h) {
       mbar_init(&hs_full[h], 1);
       mbar_init(&hs_empty[h], 128);
@@ -179,6 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) trace_at(args, 1);
 
   if (warp == 4) {
     // ============================ TMA producer ============================
@@ -220,15 +233,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
       };
       uint32_t it = 0;
+      // b_mn: B box = {32 n, 32 k, BN/64 n-chunks} of the 3-D view {n % 32, k, n / 32} of the HWCF
+      // filter; only hi (= the raw fp32) comes by TMA, the transform warps derive lo in smem.
+      const bool bmn = args.b_mn != 0;
+      const int b_copies = (THREE_X && !bmn) ? 2 : 1;
       // A_ROWSEG boxes are exactly KW*C4 floats wide (no OOB elements -> TMA fast path): fewer bytes
       const uint32_t a_bytes = AMODE == A_GATHER ? 0u : AMODE == A_ROWSEG ? (uint32_t)args.a_row_bytes * 128u : A_TILE;
-      const uint32_t bytes = a_bytes + (BRES ? 0u : (uint32_t)((THREE_X ? 2 : 1) * C_::BHALF));
-      if (BRES) {  // whole B half of this CTA (single N tile: rows [rank*BN/2, +BN/2)), once, to the leader
+      const uint32_t bytes = a_bytes + (BRES ? 0u : (uint32_t)(b_copies * C_::BHALF));
+      if (BRES && bmn && THREE_X) {  // own B half into own smem; the transform warps split it, then signal
+        mbar_arrive_expect_tx(b_res, (uint32_t)(args.nkb * C_::BHALF));
+        for (int kb = 0; kb < args.nkb; ++kb)
+          tma_load_3d(&tmBh, b_res, smem_u32(res_hi(kb)), 0, kb * BK, (int)rank * (BN / 64));
+      } else if (BRES) {  // whole B half of this CTA (single N tile: rows [rank*BN/2, +BN/2)), once, to the leader
         const uint32_t rb = mapa(smem_u32(b_res), 0);
-        if (rank == 0) mbar_arrive_expect_tx(b_res, 2u * (uint32_t)(args.nkb * (THREE_X ? 2 : 1) * C_::BHALF));
+        if (rank == 0) mbar_arrive_expect_tx(b_res, 2u * (uint32_t)(args.nkb * b_copies * C_::BHALF));
         for (int kb = 0; kb < args.nkb; ++kb) {
-          tma_load_3d_2sm(&tmBh, rb, smem_u32(res_hi(kb)), kb * BK, (int)rank * (BN / 2), 0);
-          if (THREE_X) tma_load_3d_2sm(&tmBl, rb, smem_u32(res_lo(kb)), kb * BK, (int)rank * (BN / 2), 0);
+          if (bmn) {
+            tma_load_3d_2sm(&tmBh, rb, smem_u32(res_hi(kb)), 0, kb * BK, (int)rank * (BN / 64));
+          } else {
+            tma_load_3d_2sm(&tmBh, rb, smem_u32(res_hi(kb)), kb * BK, (int)rank * (BN / 2), 0);
+            if (THREE_X) tma_load_3d_2sm(&tmBl, rb, smem_u32(res_lo(kb)), kb * BK, (int)rank * (BN / 2), 0);
+          }
         }
       }
       if (AMODE == A_STEM) {
@@ -264,6 +289,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const int s = it % S;
           const uint32_t u = it / S;
           if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
+          if (it == 0) trace_at(args, 2);
           const int tap = AMODE == A_IM2COL ? kb / args.ncb : 0;
           const int cb = AMODE == A_IM2COL ? kb - tap * args.ncb : 0;
           if (RELAY) {
@@ -277,7 +303,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               tma_load_5d(&tmA, &ld_full[s], smem_u32(a_hi(s)), 0, wb, hb, nimg, kb);
             else if (AMODE == A_DENSE)
               tma_load_3d(&tmA, &ld_full[s], smem_u32(a_hi(s)), kb * BK, (int)m_cta, tl.bz);
-            if (!BRES) {
+            if (!BRES && bmn) {
+              tma_load_3d(&tmBh, &ld_full[s], smem_u32(b_hi(s)), 0, kb * BK, nrow / 32);
+            } else if (!BRES) {
               tma_load_3d(&tmBh, &ld_full[s], smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
               if (THREE_X) tma_load_3d(&tmBl, &ld_full[s], smem_u32(b_lo(s)), kb * BK, nrow, tl.bz);
             }
@@ -294,7 +322,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               tma_load_5d_2sm(&tmA, fb, smem_u32(a_hi(s)), 0, wb, hb, nimg, kb);
             else
               tma_load_3d_2sm(&tmA, fb, smem_u32(a_hi(s)), kb * BK, (int)m_cta, tl.bz);
-            if (!BRES) tma_load_3d_2sm(&tmBh, fb, smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
+            if (!BRES && bmn) tma_load_3d_2sm(&tmBh, fb, smem_u32(b_hi(s)), 0, kb * BK, nrow / 32);
+            else if (!BRES) tma_load_3d_2sm(&tmBh, fb, smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
           }
         }
       }
@@ -308,10 +337,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   } else if (warp == 5) {
     // ============================ MMA issuer (leader CTA) ============================
     if (rank == 0) {  // whole warp, converged: operands stay warp-uniform
-      constexpr uint32_t idesc = idesc_tf32(2 * BMC, BN);
+      const bool bmn = args.b_mn != 0;
+      const uint32_t idesc = idesc_tf32(2 * BMC, BN) | (bmn ? IDESC_B_MN : 0u);
+      // B descriptors: K-major SW128 (filter_prep's Bt) or MN-major SW128_BASE32B (b_mn: 32 k-rows x 128 B
+      // per 32-wide n chunk -> LBO 4 KB; 4-row atoms -> SBO 512 B; K=8 step = 1 KB)
+      auto bdesc = [&](const uint8_t* ptr) {
+        return bmn ? umma_desc_sw128b32_mn(smem_u32(ptr), BK * 128, 512) : umma_desc_sw128_kmajor(smem_u32(ptr));
+      };
       uint32_t it = 0, ai = 0;
       if (BRES) {
-        mbar_wait(b_res, 0);
+        mbar_wait((THREE_X && bmn) ? b_ready : b_res, 0);
         tc_fence_after();
       }
       for (int t = cid; t < args.total_tiles; t += ncl, ++ai) {
@@ -325,31 +360,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const int s = it % S;
           mbar_wait(&full[s], (it / S) & 1);
           tc_fence_after();
+          if (it == 0 && lane == 0) trace_at(args, 3);
           const uint64_t dah = AMODE == A_NARROW ? umma_desc_interleave_kmajor(smem_u32(a_hi(s)), 2048, 128)
                                                  : umma_desc_sw128_kmajor(smem_u32(a_hi(s)));
-          const uint64_t dbh = umma_desc_sw128_kmajor(smem_u32(BRES ? res_hi(kb) : b_hi(s)));
+          const uint64_t dbh = bdesc(BRES ? res_hi(kb) : b_hi(s));
           const int l = (THREE_X && !C_::LO_TMEM) ? (int)(it % SL) : 0;
           const uint32_t lo_t = tmem_base + C_::LO_COL0 + (uint32_t)(s * BK);  // LO_TMEM: stage s's lo columns
           const uint64_t dal = (!THREE_X || C_::LO_TMEM) ? 0
                                : AMODE == A_NARROW ? umma_desc_interleave_kmajor(smem_u32(a_lo(l)), 2048, 128)
                                                    : umma_desc_sw128_kmajor(smem_u32(a_lo(l)));
-          const uint64_t dbl = THREE_X ? umma_desc_sw128_kmajor(smem_u32(BRES ? res_lo(kb) : b_lo(s))) : 0;
+          const uint64_t dbl = THREE_X ? bdesc(BRES ? res_lo(kb) : b_lo(s)) : 0;
 #pragma unroll
           for (int k = 0; k < BK / 8; ++k) {
             const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);
+            const uint64_t adv_b = bmn ? (uint64_t)((k * 1024) >> 4) : adv;
             // narrow A: one K=8 step = two 16-byte core-matrix columns = 2 boxes = 4 KB
             const uint64_t adv_a = AMODE == A_NARROW ? (uint64_t)((k * 4096) >> 4) : adv;
             const uint32_t accum = (kb > tl.kb0 || k > 0) ? 1u : 0u;
             if (THREE_X && C_::LO_TMEM) {
-              mma_tf32_2sm_ts_warp(d, lo_t + (uint32_t)(k * 8), dbh + adv, idesc, accum);
-              mma_tf32_2sm_warp(d, dah + adv_a, dbl + adv, idesc, 1u);
-              mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv, idesc, 1u);
+              mma_tf32_2sm_ts_warp(d, lo_t + (uint32_t)(k * 8), dbh + adv_b, idesc, accum);
+              mma_tf32_2sm_warp(d, dah + adv_a, dbl + adv_b, idesc, 1u);
+              mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv_b, idesc, 1u);
             } else if (THREE_X) {
-              mma_tf32_2sm_warp(d, dal + adv_a, dbh + adv, idesc, accum);
-              mma_tf32_2sm_warp(d, dah + adv_a, dbl + adv, idesc, 1u);
-              mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv, idesc, 1u);
+              mma_tf32_2sm_warp(d, dal + adv_a, dbh + adv_b, idesc, accum);
+              mma_tf32_2sm_warp(d, dah + adv_a, dbl + adv_b, idesc, 1u);
+              mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv_b, idesc, 1u);
             } else {
-              mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv, idesc, accum);
+              mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv_b, idesc, accum);
             }
           }
           mma_commit_2sm_mc_warp(&empty[s], 0x3);
@@ -365,6 +402,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const int j = t & 7;    // 16-byte chunk within the 128-byte k-row
     const int rb = t >> 3;  // rows rb + 16 i
     const uint32_t full_leader = mapa(smem_u32(full), 0);  // full[0] in the leader CTA
+    const bool bmn_lo = THREE_X && args.b_mn != 0;
+
+    // lo = x - trunc_tf32(x) over `bytes` of B hi at `hi`, written at the same offsets from `lo_dst`
+    // (elementwise: the swizzled MN-major layout carries over)
+    auto split_b = [&](const uint8_t* hi, uint8_t* lo_dst, int nbytes) {
+      const uint32_t h = smem_u32(hi), l = smem_u32(lo_dst);
+      for (int i = t * 16; i < nbytes; i += 128 * 16) {
+        const float4 v = lds128(h + (uint32_t)i);
+        sts128(l + (uint32_t)i, make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z),
+                                            v.w - tf32_hi(v.w)));
+      }
+    };
+    if (BRES && bmn_lo) {  // resident B: split every k-block once, then tell the leader's MMA warp
+      mbar_wait(b_res, 0);
+      split_b(res_hi(0), res_lo(0), args.nkb * C_::BHALF);
+      fence_proxy_async_smem();
+      mbar_arrive_remote(mapa(smem_u32(b_ready), 0));
+    }
 
     auto finalize = [&](uint32_t jt) {
       const int s = jt % S;
@@ -402,6 +457,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                                        v.w - tf32_hi(v.w)));
         }
       }
+      if (!BRES && bmn_lo) split_b(b_hi(s), b_lo(s), C_::BHALF);
       fence_proxy_async_smem();
       mbar_arrive_remote(full_leader + (uint32_t)(s * sizeof(uint64_t)));
     };
@@ -527,6 +583,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       const int acc = ai & 1;
       mbar_wait(&tmem_full[acc], (ai >> 1) & 1);
       tc_fence_after();
+      if (ai == 0 && q == 2 && lane == 0) trace_at(args, 4);
       int64_t row0 = (int64_t)tl.mi * 2 * BMC + rank * BMC + q * 32;
       int64_t m = row0 + lane;
       int sw0 = 0, sh0 = 0, sn = 0;  // A_ROWSEG / A_STEM: this warp's 16 x 2 spatial block
@@ -612,7 +669,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         }
       }
     }
+    if (q == 2 && lane == 0) trace_at(args, 5);
     if (args.tma_store == 1 && lane == 0) bulk_wait<0>();
+    if (q == 2 && lane == 0) trace_at(args, 6);
   }
 
   tc_fence_before();
@@ -621,7 +680,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     tmem_dealloc_2sm<C_::TMEM_COLS>(tmem_base);
   }
+  if (threadIdx.x == 0) trace_at(args, 7);
 }
+
+// ------------------------------------------------------------------ host: debug trace
+unsigned long long* g_trace_buf = nullptr;  // 2 * 74 CTAs x TRACE_SLOTS, device
+bool g_trace_on = false;
 
 // ------------------------------------------------------------------ host: tensor maps
 PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
@@ -756,6 +820,12 @@ cudaError_t launch_bn(int bn, const CUtensorMap& a, const CUtensorMap& bh, const
 
 bool gemm2_encode_tiled(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
                         const uint32_t* box, bool swizzle128) {
+  return gemm2_encode_tiled_sw(m, rank, base, dims, strides, box,
+                               swizzle128 ? (int)CU_TENSOR_MAP_SWIZZLE_128B : (int)CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+bool gemm2_encode_tiled_sw(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
+                           const uint32_t* box, int swizzle) {
   if (load_driver_fns() != cudaSuccess) return false;
   cuuint64_t d[5], st[4];
   cuuint32_t b[5], es[5];
@@ -766,8 +836,25 @@ bool gemm2_encode_tiled(CUtensorMap* m, int rank, const void* base, const uint64
     if (i < rank - 1) st[i] = strides[i];
   }
   return g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), d, st, b, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, (CUtensorMapSwizzle)swizzle,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int gemm2_trace(int enable, unsigned long long* host, int n) {
+  if (enable >= 0) {
+    if (enable && !g_trace_buf &&
+        cudaMalloc(&g_trace_buf, 148 * TRACE_SLOTS * sizeof(unsigned long long)) != cudaSuccess)
+      return -1;
+    if (enable && g_trace_buf) cudaMemset(g_trace_buf, 0, 148 * TRACE_SLOTS * sizeof(unsigned long long));
+    g_trace_on = enable != 0;
+  }
+  if (host && g_trace_buf) {
+    const int m = n < 148 * TRACE_SLOTS ? n : 148 * TRACE_SLOTS;
+    if (cudaMemcpy(host, g_trace_buf, (size_t)m * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+      return -1;
+    return m;
+  }
+  return 0;
 }
 
 int gemm2_choose_block_n(int64_t N) {
@@ -848,6 +935,8 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   if (tiles > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
   a.total_tiles = (int)tiles;
   a.d = g.d; a.ldd = g.ldd; a.d_bstride = g.d_batch_stride; a.partial = g.partial;
+  a.trace = g_trace_on ? g_trace_buf : nullptr;
+  a.b_mn = g.b_mn ? 1 : 0;
 
   alignas(64) CUtensorMap ta{}, tbh{}, tbl{};
   bool ok = true;
@@ -861,8 +950,18 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
     ok = gemm2_encode_tiled(&ta, 3, g.gather_x, dims, st, box, false);
   }
   else if (g.a_mode == A_DENSE) ok = make_tiled_3d(&ta, g.a, g.a_k, g.M, g.batch, g.lda, BMC);
-  ok = ok && make_tiled_3d(&tbh, g.bt_hi, g.kpad, g.npad, g.batch, g.kpad, g.block_n / 2);
-  if (g.three_x) ok = ok && make_tiled_3d(&tbl, g.bt_lo, g.kpad, g.npad, g.batch, g.kpad, g.block_n / 2);
+  if (g.b_mn) {
+    // B straight from the row-major (b_rows x N) filter: 3-D view {n % 32, k, n / 32}; box {32, 32, BN/64}
+    if (g.N % 32 != 0 || g.batch != 1 || !g.b_w) return cudaErrorInvalidValue;
+    const uint64_t dims[3] = {32, (uint64_t)g.b_rows, (uint64_t)(g.N / 32)};
+    const uint64_t st[2] = {(uint64_t)g.N * 4, 128};
+    const uint32_t box[3] = {32, 32, (uint32_t)(g.block_n / 64)};
+    ok = ok && gemm2_encode_tiled_sw(&tbh, 3, g.b_w, dims, st, box, (int)CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    tbl = tbh;
+  } else {
+    ok = ok && make_tiled_3d(&tbh, g.bt_hi, g.kpad, g.npad, g.batch, g.kpad, g.block_n / 2);
+    if (g.three_x) ok = ok && make_tiled_3d(&tbl, g.bt_lo, g.kpad, g.npad, g.batch, g.kpad, g.block_n / 2);
+  }
   // output tensor map: dims {N, M, planes} with row stride ldd; box 32 x 32, SWIZZLE_128B
   alignas(64) CUtensorMap td{};
   a.tma_store = 0;
@@ -893,7 +992,7 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   if (g.epi_stg && a.tma_store && g.ldd % 4 == 0) a.tma_store = 2;  // tuned variant: LSU-staged stores
   if (a.tma_store != 1) td = tbh;  // unused slot
   if (g.a_mode == A_GATHER) ta = tbh;  // unused operand slot
-  if (!g.three_x) tbl = tbh;
+  if (!g.three_x || g.b_mn) tbl = tbh;
 
   const int clusters = (int)(tiles < 74 ? tiles : 74);
   if (g.three_x) {

@@ -37,6 +37,9 @@ struct Gemm2Args {
   bool three_x;
   int hp, wp;              // A_ROWSEG: padded input extent
   bool epi_stg;            // epilogue: smem-staged coalesced STG instead of TMA stores
+  bool b_mn;               // B read straight from b_w, a row-major b_rows x N matrix (the HWCF filter,
+  const float* b_w;        // k = row): MN-major operand, no filter_prep; needs N % 32 == 0, batch 1
+  int64_t b_rows;          // (bt_hi / bt_lo unused; 3xTF32 lo halves are split in smem by the kernel)
 };
 
 cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s);
@@ -48,7 +51,12 @@ bool gemm2_encode_tiled(CUtensorMap* m, int rank, const void* base, const uint64
 bool halo_ok(const Problem& p);
 cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_hi, const float* bt_lo, int64_t kpad,
                              int64_t npad, int block_n, float* out, cudaStream_t s);
+bool gemm2_encode_tiled_sw(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
+                           const uint32_t* box, int swizzle);  // swizzle: a CUtensorMapSwizzle value
 int gemm2_choose_block_n(int64_t N);
+// debug: enable (1) / disable (0) / keep (-1) per-CTA globaltimer stamps of the GEMM core (8 per CTA,
+// CTA-major, 148 CTAs max) and optionally copy them to `host` (synchronous); returns values copied.
+int gemm2_trace(int enable, unsigned long long* host, int n);
 int gemm2_choose_splits(int64_t M, int64_t N, int nkb, int batch, int block_n);
 bool gemm2_im2col_ok(const Problem& p);
 bool gemm2_narrow_ok(const Problem& p);

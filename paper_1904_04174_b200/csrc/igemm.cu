@@ -8,7 +8,8 @@
 //
 // Launch sequence (stream-ordered):
 //   [pad_channels]  only when C % 4 != 0 (e.g. the C=3 stems R1/V1)
-//   filter_prep2    W (HWCF) -> Bt (Fpad x Kpad, K-major), TF32 hi/lo split in FP32 mode
+//   [filter_prep2]  W (HWCF) -> Bt (Fpad x Kpad, K-major), TF32 hi/lo split in FP32 mode; skipped on the
+//                   im2col / dense paths with F % 32 == 0, where the GEMM reads W itself (MN-major B)
 //   gemm2sm         persistent 2-CTA tcgen05 GEMM
 //   [split_reduce]  when the pair-tile count is below one wave
 #include <cstdio>
@@ -28,6 +29,7 @@ struct Plan {
   int a_mode;
   bool three_x, pad;
   int block_n, splits, cstride, cg, rowstride, hp, wp;
+  bool b_mn;  // B straight from the HWCF filter (no filter_prep launch)
   int64_t kpad, npad;
   size_t bt_bytes, pad_bytes, partial_bytes, total;
 };
@@ -36,7 +38,10 @@ struct Plan {
 // for each algorithm"): bit 0 selects the alternative A-operand path (implicit_gemm: halo <-> im2col;
 // matmul_1x1: dense <-> im2col), bit 1 halves the N tile (256 -> 128: 3xTF32 lo halves then fit in
 // TMEM next to the accumulators, deeper TMA ring), bit 2 stores the output through the LSU
-// (smem-staged coalesced STG) instead of TMA bulk stores (frees the TMA engine for loads).
+// (smem-staged coalesced STG) instead of TMA bulk stores (frees the TMA engine for loads), bit 3 (3xTF32
+// only) routes B through filter_prep's K-major hi/lo copies instead of reading the HWCF filter directly
+// (the direct path saves a launch but splits B's lo halves in smem inside the GEMM: a win for short
+// layers, ~5-8% slower on long tensor-bound ones where smem bandwidth is the limit).
 using VKey = std::tuple<int, int, int, int, int, int, int, int, int, int, int, bool>;
 std::mutex g_vmu;
 std::map<VKey, int> g_variant;
@@ -44,7 +49,7 @@ VKey vkey(const Problem& p, bool is_1x1) {
   return VKey(p.N, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH, p.SW, p.pad_top * 64 + p.pad_left, (int)p.math, is_1x1);
 }
 int variant_of(const Problem& p, bool is_1x1) {
-  if (const char* f = getenv("CONV2D_FORCE_VARIANT")) return atoi(f) & 7;  // parity-test hook
+  if (const char* f = getenv("CONV2D_FORCE_VARIANT")) return atoi(f) & 15;  // parity-test hook
   std::lock_guard<std::mutex> lk(g_vmu);
   auto it = g_variant.find(vkey(p, is_1x1));
   return it == g_variant.end() ? 0 : it->second;
@@ -102,7 +107,11 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
   pl.kpad = rowk ? (int64_t)p.KH * 32 : round_up((int64_t)p.KH * p.KW * pl.cstride, 32);
   pl.splits = (p.F % 4 == 0 && !rowk && pl.a_mode != A_HALO)
                   ? gemm2_choose_splits(p.M(), p.F, (int)(pl.kpad / 32), 1, pl.block_n) : 1;
-  pl.bt_bytes = round_up((int64_t)pl.npad * pl.kpad * 4, 256);
+  // HWCF rows are exactly the GEMM's k order for the im2col (C % 32 == 0: k = tap*C + c) and dense 1x1
+  // (k = c) paths, so the GEMM reads W as an MN-major B operand -- no filter_prep launch, no Bt copy
+  pl.b_mn = (pl.a_mode == A_IM2COL || pl.a_mode == A_DENSE) && p.F % 32 == 0 &&
+            !((variant & 8) && pl.three_x) && getenv("CONV2D_NO_BMN") == nullptr;
+  pl.bt_bytes = pl.b_mn ? 0 : round_up((int64_t)pl.npad * pl.kpad * 4, 256);
   pl.pad_bytes = !pl.pad ? 0
                  : rowk ? round_up((int64_t)p.N * pl.hp * pl.wp * pl.cg * 4, 256)
                                          : round_up((int64_t)p.N * p.H * p.W * pl.cg * 4, 256);
@@ -117,12 +126,17 @@ int igemm_variants(const Problem& p, bool is_1x1, int* masks) {
                             : ((halo_ok(p) && gemm2_im2col_ok(p)) ||
                                (gemm2_rowseg_ok(p) && gemm2_stem_ok(p, gemm2_choose_block_n(p.F), p.math == 0)));
   const bool alt_n = gemm2_choose_block_n(p.F) == 256;
+  // bit 3 matters only where some A path reads B directly (im2col / dense, F % 32 == 0) in 3xTF32 mode
+  const bool alt_b = p.math == CONV2D_MATH_FP32 && p.F % 32 == 0 &&
+                     ((is_1x1 && p.C % 4 == 0 && p.C >= 32) || gemm2_im2col_ok(p));
   int n = 0;
-  // bit 0: A path, bit 1: N tile.  Bit 2 (LSU-staged epilogue) is not enumerated: it measured slower
-  // than TMA stores on every paper layer (kept reachable through CONV2D_FORCE_VARIANT for experiments).
-  for (int m = 0; m < 4; ++m) {
+  // bit 0: A path, bit 1: N tile, bit 3: B path.  Bit 2 (LSU-staged epilogue) is not enumerated: it
+  // measured slower than TMA stores on every paper layer (reachable through CONV2D_FORCE_VARIANT).
+  for (int m = 0; m < 16; ++m) {
+    if (m & 4) continue;
     if ((m & 1) && !alt_a) continue;
     if ((m & 2) && !alt_n) continue;
+    if ((m & 8) && !alt_b) continue;
     if (masks) masks[n] = m;
     ++n;
   }
@@ -136,7 +150,7 @@ void igemm_set_variant(const Problem& p, bool is_1x1, int v) {
 
 size_t igemm_workspace(const Problem& p, bool is_1x1) {
   size_t w = 0;
-  int masks[8];
+  int masks[16];
   const int n = igemm_variants(p, is_1x1, masks);
   for (int i = 0; i < n; ++i) w = std::max(w, make_plan(p, is_1x1, masks[i]).total);
   return w;
@@ -144,7 +158,7 @@ size_t igemm_workspace(const Problem& p, bool is_1x1) {
 
 int igemm_launches(const Problem& p, bool is_1x1) {
   const Plan pl = make_plan(p, is_1x1, variant_of(p, is_1x1));
-  return 2 + (pl.pad ? 1 : 0) + (pl.splits > 1 ? 1 : 0);
+  return (pl.b_mn ? 1 : 2) + (pl.pad ? 1 : 0) + (pl.splits > 1 ? 1 : 0);
 }
 
 cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const float* filt, float* out, void* ws,
@@ -175,9 +189,11 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
     xg = xp;
   }
   float* partial = pl.splits > 1 ? reinterpret_cast<float*>(w8) : nullptr;
-  cudaError_t e =
-      launch_filter_prep2(filt, p.KH, p.KW, p.C, p.F, pl.cstride, pl.rowstride, pl.kpad, pl.npad, bt_hi, bt_lo, s);
-  if (e != cudaSuccess) return e;
+  if (!pl.b_mn) {
+    cudaError_t e =
+        launch_filter_prep2(filt, p.KH, p.KW, p.C, p.F, pl.cstride, pl.rowstride, pl.kpad, pl.npad, bt_hi, bt_lo, s);
+    if (e != cudaSuccess) return e;
+  }
   if (pl.a_mode == A_HALO) return launch_gemm_halo(p, in, bt_hi, bt_lo, pl.kpad, pl.npad, pl.block_n, out, s);
   Gemm2Args g{};
   g.a_mode = pl.a_mode;
@@ -203,6 +219,9 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
   g.hp = pl.hp;
   g.wp = pl.wp;
   g.epi_stg = (variant_of(p, is_1x1) & 4) != 0;
+  g.b_mn = pl.b_mn;
+  g.b_w = filt;
+  g.b_rows = (int64_t)p.KH * p.KW * p.C;
   return launch_gemm2(p, g, s);
 }
 

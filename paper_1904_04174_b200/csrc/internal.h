@@ -47,4 +47,6 @@ cudaError_t launch_synth_fill(float* dst, uint64_t count, uint64_t key, uint64_t
 cudaError_t launch_split_reduce(const float* partial, float* d, int64_t rows, int64_t cols, int64_t ldd,
                                 int splits, cudaStream_t s);
 
+int gemm2_trace(int enable, unsigned long long* host, int n);  // gemm2sm.cu (conv2d_debug.h)
+
 }  // namespace conv2d

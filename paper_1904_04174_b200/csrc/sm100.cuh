@@ -131,6 +131,22 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_kmajor(uint32_t smem_addr) {
   return d;
 }
 
+// MN-major tf32 operand (e.g. B read straight from a row-major K x N matrix).  For 32-bit MN-major
+// operands the only smem layout is SWIZZLE_128B_BASE32B (descriptor layout type 1; TMA's
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 128-byte rows = one k each, 32 consecutive n; 32-byte chunks
+// swizzled over a 4-row (512 B) atom.  LBO = byte stride between 32-wide n chunks, SBO = byte stride
+// between 4-row k groups.
+__device__ __forceinline__ uint64_t umma_desc_sw128b32_mn(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1u << 46;  // version = 1 (sm_100)
+  d |= (uint64_t)1u << 61;  // SWIZZLE_128B_BASE32B
+  return d;
+}
+constexpr uint32_t IDESC_B_MN = 1u << 16;  // instruction descriptor: B operand MN-major
+
 __host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N) {
   return (1u << 4)            // D = f32
          | (2u << 7)          // A = tf32
@@ -153,6 +169,11 @@ __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__flo
 // ====================================================================== cluster / 2-CTA extensions
 namespace sm100 {
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));

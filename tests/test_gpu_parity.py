@@ -120,6 +120,14 @@ EDGE = [
     (2, 23, 19, 3, 64, 7, 7, 2, 2, 0),
     (1, 20, 21, 5, 24, 3, 3, 1, 2, 1),
     (3, 11, 12, 8, 16, 4, 4, 2, 1, 0),
+    # direct-B path (B read from the HWCF filter as an MN-major operand, F % 32 == 0): a single 32-wide
+    # n chunk (the pair's second half out of range), a ragged last chunk pair, a K tail in the dense
+    # 1x1 path (C = 48), BN = 256 with a partial N tile, im2col with stride 2 and SAME corners
+    (2, 9, 11, 64, 32, 1, 1, 1, 1, 0),
+    (1, 12, 10, 64, 96, 3, 3, 2, 2, 0),
+    (2, 10, 10, 48, 64, 1, 1, 1, 1, 0),
+    (1, 6, 40, 64, 288, 1, 1, 1, 1, 0),
+    (1, 15, 13, 128, 160, 3, 3, 2, 2, 0),
 ]
 
 
@@ -216,7 +224,7 @@ def test_tf32_mma_reads_truncated_operands(cuda_ok):
     assert np.array_equal(gpu_conv(p, x, w, a), gpu_conv(p, xt, wt, a))
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 7])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 7, 8, 11])
 @pytest.mark.parametrize("case", [(2, 28, 28, 64, 64, 3, 3, 1, 1, 0), (1, 14, 15, 128, 128, 3, 3, 1, 1, 1),
                                   (2, 12, 12, 64, 256, 1, 1, 1, 1, 0), (1, 9, 9, 64, 320, 3, 3, 2, 2, 0),
                                   (2, 21, 19, 3, 36, 7, 7, 2, 2, 0)], ids=str)

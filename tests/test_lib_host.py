@@ -25,7 +25,8 @@ def C():
 
 
 def test_exports_every_declared_symbol(C):
-    hdr = open(os.path.join(ROOT, "include", "conv2d.h")).read()
+    inc = os.path.join(ROOT, "include")
+    hdr = "".join(open(os.path.join(inc, f)).read() for f in sorted(os.listdir(inc)) if f.endswith(".h"))
     declared = set(re.findall(r"\b(conv2d_[a-z_]+)\s*\(", hdr))
     declared = {d for d in declared if not d.endswith("_t")}
     assert declared == set(C.EXPORTED), declared ^ set(C.EXPORTED)

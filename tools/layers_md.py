@@ -29,7 +29,8 @@ def main():
         # which algorithm wins how often (the paper's "no single algorithm always performing best")
         wins = {}
         for r in d["layers"]:
-            best = min((a for a in r["algos"] if a != "auto"), key=lambda a: r["algos"][a]["best_us"])
+            cand = [a for a in r["algos"] if a != "auto"] or list(r["algos"])
+            best = min(cand, key=lambda a: r["algos"][a]["best_us"])
             wins[best] = wins.get(best, 0) + 1
         print("\nFastest algorithm per layer: " + ", ".join(f"{k} x{v}" for k, v in sorted(wins.items())) + "\n")
 
