@@ -190,6 +190,46 @@ def workload_config(args, per_gpu):
 
 
 # ----------------------------------------------------------------------------- our arm
+def step_trace(args, C, convs, ws, flush):
+    """One extra, untimed replay of the step captured with the GEMM-kernel trace on: per launch (= per
+    conv), the CTA entry/setup/first-MMA/exit stamps relative to the step's first entry."""
+    import torch
+    C.conv2d_debug_trace(1)
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
+        cs = torch.cuda.current_stream()
+        for cv in convs:
+            C.conv2d_forward(cv["p"], C.ALGO_AUTO, cv["x"], cv["w"], cv["y"], ws, ws.numel(), cs)
+    C.conv2d_debug_trace(0)
+    flush.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    t = C.conv2d_debug_trace(-1, read=True)
+    rec = 148 * 8
+    out, t0, prev_end = [], None, None
+    for i, cv in enumerate(convs):
+        r = t[i * rec:(i + 1) * rec]
+        ctas = [r[j * 8:(j + 1) * 8] for j in range(148) if r[j * 8] != 0]
+        if not ctas:
+            continue
+        start = min(c[0] for c in ctas)
+        t0 = start if t0 is None else t0
+        end = max(c[7] for c in ctas)
+        med = lambda k: statistics.median([c[k] for c in ctas if c[k]]) if any(c[k] for c in ctas) else None
+        ent = {"conv": i, "layer": cv["layer"].name, "algo": C.ALGO_NAMES[cv["algo"]], "ctas": len(ctas),
+               "start_us": round((start - t0) / 1e3, 2), "span_us": round((end - start) / 1e3, 2),
+               "gap_before_us": round((start - prev_end) / 1e3, 2) if prev_end else None}
+        for k, nm in ((1, "setup"), (3, "mma0"), (5, "last_store")):
+            m = med(k)
+            ent[nm + "_med_us"] = round((m - start) / 1e3, 2) if m else None
+        ent["exit_med_us"] = round((med(7) - start) / 1e3, 2)
+        out.append(ent)
+        prev_end = end
+    with open(args.trace_out, "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -203,6 +243,8 @@ def main():
     ap.add_argument("--global-batch", type=int, default=GLOBAL_BATCH,
                     help="analysis only (default = BASELINE config 5's 256)")
     ap.add_argument("--layers-out", default="", help="write the per-layer table (JSON) here")
+    ap.add_argument("--trace-out", default="", help="diagnostics: per-launch GEMM timeline of one extra "
+                    "(untimed) graph replay of the step, JSON (include/conv2d_debug.h)")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
@@ -416,6 +458,9 @@ def main():
         del r["ms"]
 
     launches = sum(cv["launches"] for cv in convs) * args.steps
+
+    if args.trace_out and rank == 0:
+        step_trace(args, C, convs, ws, flush)
 
     # ---- end to end through the public API: pinned host -> device, forward, device -> host
     e2e = None

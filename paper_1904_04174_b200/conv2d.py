@@ -211,9 +211,9 @@ def conv2d_last_error() -> str:
 
 
 def conv2d_debug_trace(enable: int, read: bool = False) -> list:
-    """include/conv2d_debug.h: toggle the GEMM core's per-CTA globaltimer stamps; with read=True
-    returns the 148 x 8 stamps (ns) as a flat list."""
-    n = 148 * 8
+    """include/conv2d_debug.h: toggle the GEMM kernels' per-CTA globaltimer stamps; with read=True
+    returns the 256 launch records x 148 CTAs x 8 stamps (ns) as a flat list."""
+    n = 256 * 148 * 8
     buf = (ctypes.c_ulonglong * n)() if read else None
     got = _lib.conv2d_debug_trace(int(enable), buf, n if read else 0)
     if got < 0:

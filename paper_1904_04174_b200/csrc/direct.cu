@@ -8,6 +8,8 @@
 // (no data reuse beyond L1/L2) -- the baseline the other algorithms beat.
 #include "internal.h"
 
+#include "launch.cuh"
+
 namespace conv2d {
 namespace {
 
@@ -16,6 +18,8 @@ __global__ void __launch_bounds__(256) direct_kernel(const float* __restrict__ i
                                                      float* __restrict__ out, int H, int W, int C, int F, int KH,
                                                      int KW, int SH, int SW, int HO, int WO, int PT, int PL,
                                                      int64_t total) {
+  pdl_trigger();
+  pdl_wait();
   const int FQ = (F + 3) / 4;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int fq = (int)(t % FQ);
@@ -70,13 +74,9 @@ cudaError_t launch_direct(const Problem& p, const float* in, const float* filt, 
   const int threads = 256;
   int64_t blocks = (total + threads - 1) / threads;
   if (blocks > 148LL * 64) blocks = 148LL * 64;  // grid-stride beyond ~64 resident-block waves
-  if (p.F % 4 == 0)
-    direct_kernel<true><<<(unsigned)blocks, threads, 0, s>>>(in, filt, out, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH,
-                                                             p.SW, p.HO, p.WO, p.pad_top, p.pad_left, total);
-  else
-    direct_kernel<false><<<(unsigned)blocks, threads, 0, s>>>(in, filt, out, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH,
-                                                              p.SW, p.HO, p.WO, p.pad_top, p.pad_left, total);
-  return cudaGetLastError();
+  auto kern = p.F % 4 == 0 ? direct_kernel<true> : direct_kernel<false>;
+  return launch_k(kern, dim3((unsigned)blocks), dim3(threads), 0, s, in, filt, out, p.H, p.W, p.C, p.F, p.KH, p.KW,
+                  p.SH, p.SW, p.HO, p.WO, p.pad_top, p.pad_left, total);
 }
 
 }  // namespace conv2d

@@ -31,6 +31,7 @@
 #include <mutex>
 
 #include "gemm2sm.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace conv2d {
@@ -58,6 +59,7 @@ struct DevArgs {
   int64_t ldd, d_bstride;
   float* partial;
   int tma_store;  // 1: epilogue stages 32x32 chunks in smem and writes them with TMA stores
+  int bstat;  // B-stationary schedule (B-resident with several N tiles): pair p owns N tile p % nt
   int b_mn;  // 1: B read straight from the row-major K x F filter (MN-major operand; no filter_prep)
   unsigned long long* trace;  // debug (conv2d_debug_trace): TRACE_SLOTS globaltimer stamps per CTA, or null
 };
@@ -110,6 +112,20 @@ __device__ __forceinline__ Tile decode(const DevArgs& a, int t) {
   return r;
 }
 
+// The j-th tile of CTA pair `cid` (of ncl), or -1.  Default: static round-robin over all tiles.
+// B-stationary (args.bstat): pair cid owns N tile ni = cid % nt and walks that tile column's M tiles
+// with stride = the number of pairs owning ni, so the pair's resident B half serves every tile it runs.
+__device__ __forceinline__ int tile_at(const DevArgs& a, int cid, int ncl, int j) {
+  if (!a.bstat) {
+    const int64_t t = (int64_t)cid + (int64_t)j * ncl;
+    return t < a.total_tiles ? (int)t : -1;
+  }
+  const int ni = cid % a.nt;
+  const int owners = (ncl - ni + a.nt - 1) / a.nt;
+  const int64_t mi = (int64_t)(cid / a.nt) + (int64_t)j * owners;
+  return mi < a.mt ? (int)(mi * a.nt + ni) : -1;
+}
+
 template <int BN, bool THREE_X, int AMODE, bool BRES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     gemm2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
@@ -154,6 +170,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   const int cid = (int)cluster_id_x();
   const int ncl = (int)nclusters_x();
   if (threadIdx.x == 0) trace_at(args, 0);
+  pdl_trigger();  // launch.cuh: the next kernel may start its prologue while this one runs
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -191,6 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // first global-memory access below: the previous kernel has completed
   if (threadIdx.x == 0) trace_at(args, 1);
 
   if (warp == 4) {
@@ -240,25 +258,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       // A_ROWSEG boxes are exactly KW*C4 floats wide (no OOB elements -> TMA fast path): fewer bytes
       const uint32_t a_bytes = AMODE == A_GATHER ? 0u : AMODE == A_ROWSEG ? (uint32_t)args.a_row_bytes * 128u : A_TILE;
       const uint32_t bytes = a_bytes + (BRES ? 0u : (uint32_t)(b_copies * C_::BHALF));
+      // BRES: this CTA's B half of the pair's N tile (tile ni: rows [ni*BN + rank*BN/2, +BN/2)), once
+      const int res_row = (args.bstat ? (cid % args.nt) * BN : 0) + (int)rank * (BN / 2);
       if (BRES && bmn && THREE_X) {  // own B half into own smem; the transform warps split it, then signal
         mbar_arrive_expect_tx(b_res, (uint32_t)(args.nkb * C_::BHALF));
         for (int kb = 0; kb < args.nkb; ++kb)
-          tma_load_3d(&tmBh, b_res, smem_u32(res_hi(kb)), 0, kb * BK, (int)rank * (BN / 64));
-      } else if (BRES) {  // whole B half of this CTA (single N tile: rows [rank*BN/2, +BN/2)), once, to the leader
+          tma_load_3d(&tmBh, b_res, smem_u32(res_hi(kb)), 0, kb * BK, res_row / 32);
+      } else if (BRES) {  // to the leader's barrier
         const uint32_t rb = mapa(smem_u32(b_res), 0);
         if (rank == 0) mbar_arrive_expect_tx(b_res, 2u * (uint32_t)(args.nkb * b_copies * C_::BHALF));
         for (int kb = 0; kb < args.nkb; ++kb) {
           if (bmn) {
-            tma_load_3d_2sm(&tmBh, rb, smem_u32(res_hi(kb)), 0, kb * BK, (int)rank * (BN / 64));
+            tma_load_3d_2sm(&tmBh, rb, smem_u32(res_hi(kb)), 0, kb * BK, res_row / 32);
           } else {
-            tma_load_3d_2sm(&tmBh, rb, smem_u32(res_hi(kb)), kb * BK, (int)rank * (BN / 2), 0);
-            if (THREE_X) tma_load_3d_2sm(&tmBl, rb, smem_u32(res_lo(kb)), kb * BK, (int)rank * (BN / 2), 0);
+            tma_load_3d_2sm(&tmBh, rb, smem_u32(res_hi(kb)), kb * BK, res_row, 0);
+            if (THREE_X) tma_load_3d_2sm(&tmBl, rb, smem_u32(res_lo(kb)), kb * BK, res_row, 0);
           }
         }
       }
       if (AMODE == A_STEM) {
         uint32_t u = 0;
-        for (int t = cid; t < args.total_tiles; t += ncl, ++u) {
+        for (int t, jj = 0; (t = tile_at(args, cid, ncl, jj)) >= 0; ++jj, ++u) {
           const Tile tl = decode(args, t);
           const int wo0 = (tl.mi % args.wblk) * 16;
           const int ho0 = ((tl.mi / args.wblk) % args.hblk) * 16 + (int)rank * 8;
@@ -269,7 +289,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                       tl.mi / (args.wblk * args.hblk));
         }
       }
-      for (int t = cid; t < args.total_tiles && AMODE != A_STEM; t += ncl) {
+      for (int t, jj = 0; AMODE != A_STEM && (t = tile_at(args, cid, ncl, jj)) >= 0; ++jj) {
         const Tile tl = decode(args, t);
         const int64_t m_cta = (int64_t)tl.mi * 2 * BMC + rank * BMC;
         int wb = 0, hb = 0, nimg = 0;
@@ -349,7 +369,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         mbar_wait((THREE_X && bmn) ? b_ready : b_res, 0);
         tc_fence_after();
       }
-      for (int t = cid; t < args.total_tiles; t += ncl, ++ai) {
+      for (int t, jj = 0; (t = tile_at(args, cid, ncl, jj)) >= 0; ++jj, ++ai) {
         const Tile tl = decode(args, t);
         const int acc = ai & 1;
         const uint32_t ua = ai >> 1;
@@ -463,7 +483,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     };
 
     uint32_t it = 0;
-    for (int tt = cid; tt < args.total_tiles; tt += ncl) {
+    for (int tt, jj = 0; (tt = tile_at(args, cid, ncl, jj)) >= 0; ++jj) {
       const Tile tl = decode(args, tt);
       if (AMODE == A_GATHER) {
         int ihb[8], iwb[8];
@@ -513,7 +533,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         // thread t builds A row t = (ho_l, wo_l) = (t / 16, t % 16) of this CTA's 16x8 tile: for kernel
         // row r, the KW*C4 contiguous halo floats at halo row ho_l*SH + r, column wo_l*SW*C4; the
         // remaining chunks of the 128-B row stay zero (cleared at kernel start).
-        const uint32_t uh = (uint32_t)((tt - cid) / ncl);
+        const uint32_t uh = (uint32_t)jj;
         const int h = uh & 1;
         mbar_wait(&hs_full[h], (uh >> 1) & 1);
         const uint32_t hbase = smem_u32(halo + h * 16384) +
@@ -578,7 +598,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const uint32_t ebuf = smem_u32(epi_smem) + (uint32_t)(q * 2 * 4096);
     if (args.tma_store == 1 && lane == 0) tma_prefetch(&tmD);
     uint32_t ai = 0, chunk = 0;
-    for (int t = cid; t < args.total_tiles; t += ncl, ++ai) {
+    for (int t, jj = 0; (t = tile_at(args, cid, ncl, jj)) >= 0; ++jj, ++ai) {
       const Tile tl = decode(args, t);
       const int acc = ai & 1;
       mbar_wait(&tmem_full[acc], (ai >> 1) & 1);
@@ -684,8 +704,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 }
 
 // ------------------------------------------------------------------ host: debug trace
-unsigned long long* g_trace_buf = nullptr;  // 2 * 74 CTAs x TRACE_SLOTS, device
+constexpr int TRACE_LAUNCHES = 256;           // ring of launch records
+constexpr int TRACE_RECORD = 148 * TRACE_SLOTS;  // one record: 148 CTAs x TRACE_SLOTS stamps
+unsigned long long* g_trace_buf = nullptr;       // TRACE_LAUNCHES records, device
 bool g_trace_on = false;
+int g_trace_next = 0;
 
 // ------------------------------------------------------------------ host: tensor maps
 PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
@@ -783,16 +806,18 @@ cudaError_t launch_t(const CUtensorMap& a, const CUtensorMap& bh, const CUtensor
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<dim3(2 * clusters), NTHREADS, C_::SMEM, s>>>(a, bh, bl, dm, args);
-  return cudaGetLastError();
+  return launch_k(kern, dim3(2 * clusters), dim3(NTHREADS), C_::SMEM, s, a, bh, bl, dm, args);
 }
 
 template <bool THREE_X, int AMODE>
 cudaError_t launch_bn(int bn, const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl,
                       const CUtensorMap& dm, const DevArgs& args, int clusters, cudaStream_t s) {
-  // BRES: one N tile, no split-K / batching, and every k-block of this CTA's B half fits the region
+  // BRES: no split-K / batching, every k-block of this CTA's B half fits the region, and one N tile --
+  // or several with the B-stationary schedule (args.bstat, set by the caller when every N tile gets a
+  // pair: tiles >= 74 pairs)
   const bool bres = AMODE == A_STEM ||
-                    (args.nt == 1 && args.splits == 1 && args.batch == 1 && getenv("CONV2D_NO_BRES") == nullptr &&
+                    ((args.nt == 1 || args.bstat) && args.splits == 1 && args.batch == 1 &&
+                     getenv("CONV2D_NO_BRES") == nullptr &&
                      (AMODE == A_ROWSEG || AMODE == A_DENSE || AMODE == A_IM2COL));
   if (AMODE == A_STEM) {  // always B-resident; only instantiated where it fits (host checks gemm2_stem_ok)
     if (bn == 64) return launch_t<64, THREE_X, AMODE, true>(a, bh, bl, dm, args, clusters, s);
@@ -840,16 +865,22 @@ bool gemm2_encode_tiled_sw(CUtensorMap* m, int rank, const void* base, const uin
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+unsigned long long* gemm2_trace_record() {
+  if (!g_trace_on || !g_trace_buf) return nullptr;
+  return g_trace_buf + (size_t)(g_trace_next++ % TRACE_LAUNCHES) * TRACE_RECORD;
+}
+
 int gemm2_trace(int enable, unsigned long long* host, int n) {
+  const size_t total = (size_t)TRACE_LAUNCHES * TRACE_RECORD;
   if (enable >= 0) {
-    if (enable && !g_trace_buf &&
-        cudaMalloc(&g_trace_buf, 148 * TRACE_SLOTS * sizeof(unsigned long long)) != cudaSuccess)
+    if (enable && !g_trace_buf && cudaMalloc(&g_trace_buf, total * sizeof(unsigned long long)) != cudaSuccess)
       return -1;
-    if (enable && g_trace_buf) cudaMemset(g_trace_buf, 0, 148 * TRACE_SLOTS * sizeof(unsigned long long));
+    if (enable && g_trace_buf) cudaMemset(g_trace_buf, 0, total * sizeof(unsigned long long));
+    if (enable) g_trace_next = 0;
     g_trace_on = enable != 0;
   }
   if (host && g_trace_buf) {
-    const int m = n < 148 * TRACE_SLOTS ? n : 148 * TRACE_SLOTS;
+    const int m = (size_t)n < total ? n : (int)total;
     if (cudaMemcpy(host, g_trace_buf, (size_t)m * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
       return -1;
     return m;
@@ -935,8 +966,16 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   if (tiles > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
   a.total_tiles = (int)tiles;
   a.d = g.d; a.ldd = g.ldd; a.d_bstride = g.d_batch_stride; a.partial = g.partial;
-  a.trace = g_trace_on ? g_trace_buf : nullptr;
+  a.trace = gemm2_trace_record();
   a.b_mn = g.b_mn ? 1 : 0;
+  {  // B-stationary: several N tiles, each owned by >= 1 pair, B half resident (short K)
+    const int kbmax = g.block_n == 64 ? (g.three_x ? Cfg<64, true, true>::RES_KB_MAX : Cfg<64, false, true>::RES_KB_MAX)
+                      : g.block_n == 128 ? (g.three_x ? Cfg<128, true, true>::RES_KB_MAX : Cfg<128, false, true>::RES_KB_MAX)
+                                         : (g.three_x ? Cfg<256, true, true>::RES_KB_MAX : Cfg<256, false, true>::RES_KB_MAX);
+    static const bool bstat_env = getenv("CONV2D_BSTAT") != nullptr;
+    a.bstat = (bstat_env || g.bstat) && a.nt > 1 && g.splits == 1 && g.batch == 1 && tiles >= 74 &&
+              a.nkb <= kbmax && (g.a_mode == A_DENSE || g.a_mode == A_IM2COL) ? 1 : 0;
+  }
 
   alignas(64) CUtensorMap ta{}, tbh{}, tbl{};
   bool ok = true;

@@ -6,7 +6,7 @@
 
 namespace conv2d {
 
-enum { A_IM2COL = 0, A_DENSE = 1, A_GATHER = 2, A_NARROW = 3, A_ROWSEG = 4, A_HALO = 5, A_STEM = 6 };
+enum { A_IM2COL = 0, A_DENSE = 1, A_GATHER = 2, A_NARROW = 3, A_ROWSEG = 4, A_HALO = 5, A_STEM = 6, A_S2D = 7 };
 
 struct Gemm2Args {
   int a_mode;              // A_IM2COL: a = NHWC input (C % 32 == 0), k = (r, s, c-block of 32)
@@ -40,6 +40,7 @@ struct Gemm2Args {
   bool b_mn;               // B read straight from b_w, a row-major b_rows x N matrix (the HWCF filter,
   const float* b_w;        // k = row): MN-major operand, no filter_prep; needs N % 32 == 0, batch 1
   int64_t b_rows;          // (bt_hi / bt_lo unused; 3xTF32 lo halves are split in smem by the kernel)
+  bool bstat;              // B-stationary schedule where B-resident applies with several N tiles
 };
 
 cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s);
@@ -49,14 +50,21 @@ bool gemm2_encode_tiled(CUtensorMap* m, int rank, const void* base, const uint64
 
 // gemm_halo.cu: 3x3 stride-1 convolution with C % 32 == 0 as a halo-tile implicit GEMM (see file header)
 bool halo_ok(const Problem& p);
+// space-to-depth stem (gemm_halo.cu): K x K / stride 2, K in {7, 8}, C <= 4, F <= 128
+bool s2d_ok(const Problem& p);
+size_t s2d_workspace(const Problem& p, int block_n, bool three_x);
+cudaError_t launch_gemm_s2d(const Problem& p, const float* in, const float* filt, int block_n, bool three_x,
+                            void* ws, float* out, cudaStream_t s);
 cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_hi, const float* bt_lo, int64_t kpad,
                              int64_t npad, int block_n, float* out, cudaStream_t s);
 bool gemm2_encode_tiled_sw(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
                            const uint32_t* box, int swizzle);  // swizzle: a CUtensorMapSwizzle value
 int gemm2_choose_block_n(int64_t N);
-// debug: enable (1) / disable (0) / keep (-1) per-CTA globaltimer stamps of the GEMM core (8 per CTA,
-// CTA-major, 148 CTAs max) and optionally copy them to `host` (synchronous); returns values copied.
+// debug: enable (1) / disable (0) / keep (-1) per-CTA globaltimer stamps of the GEMM kernels (records of
+// 148 CTAs x 8 stamps, one per launch, ring of 256) and optionally copy them to `host` (synchronous);
+// returns values copied.  gemm2_trace_record(): the next launch's record, or null when disabled.
 int gemm2_trace(int enable, unsigned long long* host, int n);
+unsigned long long* gemm2_trace_record();
 int gemm2_choose_splits(int64_t M, int64_t N, int nkb, int batch, int block_n);
 bool gemm2_im2col_ok(const Problem& p);
 bool gemm2_narrow_ok(const Problem& p);

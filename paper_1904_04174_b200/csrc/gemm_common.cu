@@ -3,6 +3,7 @@
 //   pad_channels   : NHWC C -> Cp (zero channels) so 16-byte gathers stay aligned (C=3 stems)
 //   split_reduce   : deterministic fixed-order sum of split-K partial tiles
 #include "gemm2sm.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace conv2d {
@@ -15,6 +16,8 @@ namespace {
 __global__ void filter_prep2_kernel(const float* __restrict__ w, int KH, int KW, int C, int F, int cstride,
                                     int rowstride, int64_t kpad, int64_t npad, float* __restrict__ bt_hi,
                                     float* __restrict__ bt_lo) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float tile[32][33];
   const int64_t k0 = (int64_t)blockIdx.x * 32, n0 = (int64_t)blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -42,6 +45,8 @@ __global__ void filter_prep2_kernel(const float* __restrict__ w, int KH, int KW,
 // One thread per padded pixel (32-bit index math), Cp/4 float4 stores each.
 __global__ void pad_spatial_kernel(const float* __restrict__ x, int N, int H, int W, int C, int Hp, int Wp, int Cp,
                                    int pt, int pl, float* __restrict__ xp) {
+  pdl_trigger();
+  pdl_wait();
   const int total = N * Hp * Wp;
   for (int px = blockIdx.x * blockDim.x + threadIdx.x; px < total; px += gridDim.x * blockDim.x) {
     const int j = px % Wp;
@@ -63,6 +68,8 @@ __global__ void pad_spatial_kernel(const float* __restrict__ x, int N, int H, in
 
 __global__ void pad_channels_kernel(const float* __restrict__ x, int64_t pixels, int C, int Cp,
                                     float* __restrict__ xp) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = pixels * Cp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t px = i / Cp;
@@ -75,6 +82,8 @@ __global__ void pad_channels_kernel(const float* __restrict__ x, int64_t pixels,
 // fixed split order: deterministic.
 __global__ void split_reduce_kernel(const float* __restrict__ partial, float* __restrict__ d, int64_t plane4,
                                     int splits) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < plane4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 acc = reinterpret_cast<const float4*>(partial)[i];
     for (int s = 1; s < splits; ++s) {
@@ -90,8 +99,8 @@ __global__ void split_reduce_kernel(const float* __restrict__ partial, float* __
 cudaError_t launch_filter_prep2(const float* w, int KH, int KW, int C, int F, int cstride, int rowstride,
                                 int64_t kpad, int64_t npad, float* bt_hi, float* bt_lo, cudaStream_t s) {
   dim3 grid((unsigned)((kpad + 31) / 32), (unsigned)((npad + 31) / 32));
-  filter_prep2_kernel<<<grid, dim3(32, 8), 0, s>>>(w, KH, KW, C, F, cstride, rowstride, kpad, npad, bt_hi, bt_lo);
-  return cudaGetLastError();
+  return launch_k(filter_prep2_kernel, grid, dim3(32, 8), 0, s, w, KH, KW, C, F, cstride, rowstride, kpad, npad, bt_hi,
+                  bt_lo);
 }
 
 cudaError_t launch_pad_spatial(const float* x, int N, int H, int W, int C, int Hp, int Wp, int Cp, int pt, int pl,
@@ -100,16 +109,14 @@ cudaError_t launch_pad_spatial(const float* x, int N, int H, int W, int C, int H
   if (total > 0x7FFFFFFF) return cudaErrorInvalidValue;
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  pad_spatial_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, N, H, W, C, Hp, Wp, Cp, pt, pl, xp);
-  return cudaGetLastError();
+  return launch_k(pad_spatial_kernel, dim3((unsigned)blocks), dim3(256), 0, s, x, N, H, W, C, Hp, Wp, Cp, pt, pl, xp);
 }
 
 cudaError_t launch_pad_channels(const float* x, int64_t pixels, int C, int Cp, float* xp, cudaStream_t s) {
   const int64_t total = pixels * Cp;
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  pad_channels_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, pixels, C, Cp, xp);
-  return cudaGetLastError();
+  return launch_k(pad_channels_kernel, dim3((unsigned)blocks), dim3(256), 0, s, x, pixels, C, Cp, xp);
 }
 
 cudaError_t launch_split_reduce(const float* partial, float* d, int64_t rows, int64_t cols, int64_t ldd, int splits,
@@ -118,8 +125,7 @@ cudaError_t launch_split_reduce(const float* partial, float* d, int64_t rows, in
   const int64_t plane4 = rows * ldd / 4;
   int64_t blocks = (plane4 + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  split_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(partial, d, plane4, splits);
-  return cudaGetLastError();
+  return launch_k(split_reduce_kernel, dim3((unsigned)blocks), dim3(256), 0, s, partial, d, plane4, splits);
 }
 
 }  // namespace conv2d

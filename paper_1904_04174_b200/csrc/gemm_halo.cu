@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "gemm2sm.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace conv2d {
@@ -29,20 +30,46 @@ using namespace sm100;
 constexpr int BK = 32;
 constexpr int NTHREADS = 320;
 constexpr int TW = 8, TH = 16;            // CTA output tile (wo x ho) = 128 GEMM rows
-constexpr int HWD = 16, HHT = TH + 2;     // halo box: 16 (w) x 18 (h) pixels
-constexpr int HALO_ROWS = HWD * HHT;      // 288
-constexpr int HALO_BYTES = HALO_ROWS * 128;  // 36 KB (multiple of 1024)
+constexpr int HWD = 16;                   // halo box width (pixels) = 8-row group pitch
+
+// Halo geometries:
+//   G3X3 (0): 3x3 / stride 1, C % 32 == 0: halo box {32 ch, 16 w, 18 h} SWIZZLE_128B (128-byte pixel
+//             rows), one k-block (32 channels) per tap, nine k-blocks per channel block;
+//   GS2D (1): the space-to-depth stem: a 4x4 / stride-1 VALID conv over X' = s2d(x) with 16 channels
+//             (64-byte pixel rows, SWIZZLE_64B): halo box {16 ch, 16 w, 19 h}, two taps per 32-wide
+//             k-block, eight k-blocks.  (7x7 or 8x8 / stride 2 with C <= 4 maps onto it exactly.)
+enum { G3X3 = 0, GS2D = 1 };
+template <int GEOM>
+struct Geo {
+  static constexpr int TAPW = GEOM == GS2D ? 4 : 3;     // taps per filter row
+  static constexpr int HHT = TH + TAPW - 1;             // halo box height
+  static constexpr int ROWB = GEOM == GS2D ? 64 : 128;  // bytes per halo pixel
+  static constexpr int HALO_ROWS = HWD * HHT;
+  static constexpr int HALO_BYTES = (HALO_ROWS * ROWB + 1023) / 1024 * 1024;
+  static constexpr int KB_PER_UNIT = GEOM == GS2D ? 8 : 9;  // 32-wide k-blocks per (tile, channel block)
+};
 
 struct HArgs {
-  int N, H, W, HO, WO, PT, PL, ncb;
+  int N, H, W, HO, WO, PT, PL, ncb;  // GS2D: H, W, PT, PL describe X' (padding already applied: 0)
   int tiles_w, tiles_h, cta_tiles, pair_tiles, nt, total;
   int64_t M, F, ldd;
   float* d;
   int tma_store;
+  unsigned long long* trace;  // debug: conv2d_debug_trace record (stamps 0, 1, 7), or null
+  // GS2D raw mode: tmX boxes are raw input patches (RAW_ROWS rows x 32 pixels x rc channels of x, origin
+  // (2*ho0 - rpt, 2*wo0 - rpl)) and the transform warps build the swizzled s2d halo from them
+  int raw, rc, rpt, rpl;
 };
 
-template <int BN, bool THREE_X>
+constexpr int RAW_ROWS = 2 * (TH + 3);  // 38 input rows behind a 19-row s2d halo
+// a patch row = 32 pixels x C floats plus 4 floats of slack: the TMA needs the innermost box
+// coordinate 16-byte aligned, so the load starts at the aligned float below the patch origin
+__host__ __device__ constexpr int raw_row_floats(int c) { return 32 * c + 4; }
+constexpr int RAW_BYTES_MAX = RAW_ROWS * raw_row_floats(3) * 4;  // C <= 3: 15200 B
+
+template <int BN, bool THREE_X, int GEOM>
 struct HCfg {
+  static constexpr int HALO_BYTES = Geo<GEOM>::HALO_BYTES;
   static constexpr int BHALF = (BN / 2) * BK * 4;
   static constexpr int BFULL = BN * BK * 4;
   static constexpr int HS = THREE_X ? 2 : 3;                           // halo slots
@@ -55,9 +82,14 @@ struct HCfg {
   static constexpr int BSTAGE = CONCAT ? BFULL + BHALF : (THREE_X ? 2 : 1) * BHALF;
   static constexpr int ACC = CONCAT ? 2 * BN : BN;                     // TMEM columns per accumulator
   static constexpr int EPI = 4 * 2 * 32 * 128;
-  static constexpr int BUDGET = 232448 - EPI - 1024 - 512 - HS * HSLOT;
-  static constexpr int S = (BUDGET / BSTAGE) > 12 ? 12 : (BUDGET / BSTAGE);
-  static constexpr int SMEM = HS * HSLOT + S * BSTAGE + EPI + 1024 + 512;
+  static constexpr int RAWB = GEOM == GS2D ? RAW_BYTES_MAX : 0;          // raw-patch staging (one slot)
+  static constexpr int BUDGET = 232448 - EPI - RAWB - 1024 - 512 - HS * HSLOT;
+  // BRES (GS2D with CONCAT or TF32): the whole B (8 k-blocks, K = 256) stays resident -- stage kb holds
+  // k-block kb for the kernel's lifetime; otherwise B streams through an S-stage ring per unit.
+  static constexpr bool BRES = GEOM == GS2D && (CONCAT || !THREE_X);
+  static constexpr int S = BRES ? Geo<GEOM>::KB_PER_UNIT : ((BUDGET / BSTAGE) > 12 ? 12 : (BUDGET / BSTAGE));
+  static_assert(!BRES || S * BSTAGE <= BUDGET, "resident B does not fit");
+  static constexpr int SMEM = HS * HSLOT + S * BSTAGE + EPI + RAWB + 1024 + 512;
   static constexpr uint32_t TMEM_COLS = 2 * ACC;
   static_assert(S >= 2, "halo kernel needs >= 2 B stages");
   static_assert(2 * ACC <= 512, "TMEM");
@@ -77,13 +109,15 @@ __device__ __forceinline__ HTile hdecode(const HArgs& a, int t, uint32_t rank) {
   return r;
 }
 
-template <int BN, bool THREE_X>
+template <int BN, bool THREE_X, int GEOM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmBh,
                 const __grid_constant__ CUtensorMap tmBhF, const __grid_constant__ CUtensorMap tmBlF,
                 const __grid_constant__ CUtensorMap tmD,
                 const __grid_constant__ HArgs args) {
-  using C_ = HCfg<BN, THREE_X>;
+  using C_ = HCfg<BN, THREE_X, GEOM>;
+  using G_ = Geo<GEOM>;
+  constexpr int HALO_BYTES = G_::HALO_BYTES;
   constexpr int HS = C_::HS, S = C_::S;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -93,19 +127,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   auto b_x = [&](int s) { return b_z(s) + (C_::CONCAT ? C_::BFULL : 0); };                    // B_hi half
   auto b_lo = [&](int s) { return b_x(s) + C_::BHALF; };                                      // 3x, !CONCAT
   uint8_t* epi_smem = smem + (size_t)HS * C_::HSLOT + (size_t)S * C_::BSTAGE;
-  uint64_t* h_ld = reinterpret_cast<uint64_t*>(epi_smem + C_::EPI);
+  uint8_t* raw = epi_smem + C_::EPI;  // GS2D raw mode
+  uint64_t* h_ld = reinterpret_cast<uint64_t*>(raw + C_::RAWB);
   uint64_t* h_full = h_ld + HS;
   uint64_t* h_empty = h_full + HS;
   uint64_t* b_full = h_empty + HS;
   uint64_t* b_empty = b_full + S;
   uint64_t* tmem_full = b_empty + S;
   uint64_t* tmem_empty = tmem_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* raw_ld = tmem_empty + 2;     // raw patch landed (TMA -> transform)
+  uint64_t* raw_empty = raw_ld + 1;      // raw patch consumed (transform -> producer)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
-  const int taps = 9;
+  constexpr int KBU = G_::KB_PER_UNIT;
+  pdl_trigger();  // launch.cuh
+  if (threadIdx.x == 0 && args.trace) args.trace[blockIdx.x * 8 + 0] = globaltimer_ns();
 
   if (threadIdx.x == 0) {
     for (int h = 0; h < HS; ++h) {
@@ -121,6 +160,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       mbar_init(&tmem_full[a], 1);
       mbar_init(&tmem_empty[a], 2 * 128);
     }
+    mbar_init(raw_ld, 1);
+    mbar_init(raw_empty, 128);
     fence_mbar_init();
   }
   if (warp == 4 && lane == 0) {
@@ -136,6 +177,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // first global-memory access below
+  if (threadIdx.x == 0 && args.trace) args.trace[blockIdx.x * 8 + 1] = globaltimer_ns();
 
   if (warp == 4) {
     // ============================ TMA producer ============================
@@ -150,22 +193,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const int cb = u % args.ncb;
         const int h = u % HS;
         if (u >= HS) mbar_wait(&h_empty[h], ((u / HS) - 1) & 1);
-        mbar_arrive_expect_tx(&h_ld[h], HALO_BYTES);
+        if (GEOM == GS2D && args.raw) {  // raw patch; the transform warps write the halo slot
+          if (u >= 1) mbar_wait(raw_empty, (u - 1) & 1);
+          mbar_arrive_expect_tx(raw_ld, (uint32_t)(RAW_ROWS * raw_row_floats(args.rc) * 4));
+          const int col0 = (2 * tl.wo0 - args.rpl) * args.rc;
+          tma_load_3d(&tmX, raw_ld, smem_u32(raw), col0 - (col0 & 3), 2 * tl.ho0 - args.rpt, tl.n);
+          return;
+        }
+        mbar_arrive_expect_tx(&h_ld[h], (uint32_t)(G_::HALO_ROWS * G_::ROWB));  // box bytes
         tma_load_4d(&tmX, &h_ld[h], smem_u32(halo_hi(h)), cb * BK, tl.wo0 - args.PL, tl.ho0 - args.PT, tl.n);
       };
+      if (C_::BRES && units > 0) {  // all of B once (single N tile: F <= BN), to the leader's b_full[0]
+        if (rank == 0) mbar_arrive_expect_tx(&b_full[0], 2 * KBU * C_::BSTAGE);
+        for (int kb = 0; kb < KBU; ++kb) {
+          tma_load_3d_2sm(&tmBh, b_full_leader, smem_u32(b_x(kb)), kb * BK, (int)rank * (BN / 2), 0);
+          if (C_::CONCAT)
+            tma_load_3d_2sm(rank == 0 ? (const void*)&tmBhF : (const void*)&tmBlF, b_full_leader, smem_u32(b_z(kb)),
+                            kb * BK, 0, 0);
+        }
+      }
       if (units > 0) issue_halo(0);
       uint32_t bit = 0;
       for (int u = 0; u < units; ++u) {
         if (u + 1 < units) issue_halo(u + 1);
+        if (C_::BRES) continue;
         const HTile tl = hdecode(args, cid + (u / args.ncb) * ncl, rank);
         const int cb = u % args.ncb;
         const int nrow = tl.ni * BN + (int)rank * (BN / 2);
-        for (int tap = 0; tap < taps; ++tap, ++bit) {
+        for (int kb = 0; kb < KBU; ++kb, ++bit) {
           const int s = bit % S;
           if (bit >= (uint32_t)S) mbar_wait(&b_empty[s], ((bit / S) - 1) & 1);
           if (rank == 0) mbar_arrive_expect_tx(&b_full[s], 2 * C_::BSTAGE);
           const uint32_t fb = b_full_leader + (uint32_t)(s * sizeof(uint64_t));
-          const int k0 = (tap * args.ncb + cb) * BK;  // filter prep order: k = tap * C + c
+          // filter prep order k = tap * C + c: G3X3 k-block kb = tap kb, channel block cb; GS2D k-block
+          // kb = taps 2kb, 2kb+1 (16 channels each)
+          const int k0 = GEOM == GS2D ? kb * BK : (kb * args.ncb + cb) * BK;
           tma_load_3d_2sm(&tmBh, fb, smem_u32(b_x(s)), k0, nrow, 0);
           if (C_::CONCAT)  // CTA0: B_hi rows [ni*BN, +BN); CTA1: B_lo rows [ni*BN, +BN)
             tma_load_3d_2sm(rank == 0 ? (const void*)&tmBhF : (const void*)&tmBlF, fb, smem_u32(b_z(s)), k0,
@@ -174,7 +236,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             tma_load_3d_2sm(&tmBlF, fb, smem_u32(b_lo(s)), k0, nrow, 0);
         }
       }
-      for (int i = 0; i < S; ++i, ++bit)
+      for (int i = 0; i < S && !C_::BRES; ++i, ++bit)
         if (bit >= (uint32_t)S) mbar_wait(&b_empty[bit % S], ((bit / S) - 1) & 1);
       for (int i = 0; i < HS; ++i) {
         const int u = units + i;
@@ -187,6 +249,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       constexpr uint32_t idesc = idesc_tf32(256, BN);
       constexpr uint32_t idesc2 = idesc_tf32(256, 2 * BN);  // 3x: hi x [B_hi | B_lo]
       uint32_t hit = 0, bit = 0, ai = 0;
+      if (C_::BRES && cid < args.total) {
+        mbar_wait(&b_full[0], 0);
+        tc_fence_after();
+      }
       for (int t = cid; t < args.total; t += ncl, ++ai) {
         const int acc = ai & 1;
         if (ai >= 2) mbar_wait(&tmem_empty[acc], ((ai >> 1) - 1) & 1);
@@ -196,39 +262,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const int h = hit % HS;
           mbar_wait(&h_full[h], (hit / HS) & 1);
           tc_fence_after();
-          for (int tap = 0; tap < taps; ++tap, ++bit) {
-            const int s = bit % S;
-            mbar_wait(&b_full[s], (bit / S) & 1);
-            tc_fence_after();
-            const int r = tap / 3, c = tap % 3;
-            const uint32_t off = (uint32_t)((r * HWD + c) * 128);  // view start: row r*16 + c of the halo
-            // base offset stays 0: the tensor core swizzles on absolute smem address bits, so a view
-            // starting c rows into a 1024-byte period needs no descriptor correction (measured:
-            // setting the base-offset field to c breaks the integer-exact parity tests)
-            const uint64_t dah = umma_desc_sw128_kmajor_sbo(smem_u32(halo_hi(h)) + off, HWD * 128, 0u);
-            const uint64_t dal =
-                THREE_X ? umma_desc_sw128_kmajor_sbo(smem_u32(halo_lo(h)) + off, HWD * 128, 0u) : 0;
+          for (int kb = 0; kb < KBU; ++kb, ++bit) {
+            const int s = C_::BRES ? kb : (int)(bit % S);
+            if (!C_::BRES) {
+              mbar_wait(&b_full[s], (bit / S) & 1);
+              tc_fence_after();
+            }
+            // A view of tap (r, c): starts r*16 + c pixel rows into the halo; 8-row groups (one output
+            // row of 8 pixels) are 16 pixel rows apart.  Base offset stays 0: the tensor core swizzles
+            // on absolute smem address bits, so a view starting c rows into a swizzle period needs no
+            // descriptor correction (measured: setting the base-offset field breaks the exact parity).
+            auto view = [&](uint32_t base, int tap) {
+              const int r = tap / G_::TAPW, c = tap % G_::TAPW;
+              const uint32_t a = base + (uint32_t)((r * HWD + c) * G_::ROWB);
+              return GEOM == GS2D ? umma_desc_sw64_kmajor_sbo(a, HWD * G_::ROWB)
+                                  : umma_desc_sw128_kmajor_sbo(a, HWD * G_::ROWB, 0u);
+            };
+            const int tap0 = GEOM == GS2D ? 2 * kb : kb;
+            const uint64_t dah0 = view(smem_u32(halo_hi(h)), tap0);
+            const uint64_t dal0 = THREE_X ? view(smem_u32(halo_lo(h)), tap0) : 0;
+            const uint64_t dah1 = GEOM == GS2D ? view(smem_u32(halo_hi(h)), tap0 + 1) : dah0;
+            const uint64_t dal1 = (GEOM == GS2D && THREE_X) ? view(smem_u32(halo_lo(h)), tap0 + 1) : dal0;
             const uint64_t dbx = umma_desc_sw128_kmajor(smem_u32(b_x(s)));
             const uint64_t dbz = C_::CONCAT ? umma_desc_sw128_kmajor(smem_u32(b_z(s))) : 0;
             const uint64_t dbl = (THREE_X && !C_::CONCAT) ? umma_desc_sw128_kmajor(smem_u32(b_lo(s))) : 0;
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
-              const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);
-              const uint32_t accum = (cb > 0 || tap > 0 || k > 0) ? 1u : 0u;
+              const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);  // B: 32 bytes per K=8 step
+              // A: G3X3 steps through the tap's 128-byte row; GS2D takes steps 0-1 from tap 2kb's 64-byte
+              // row and steps 2-3 from tap 2kb+1's
+              const bool second = GEOM == GS2D && k >= 2;
+              const uint64_t adv_a = GEOM == GS2D ? (uint64_t)(((k & 1) * 32) >> 4) : adv;
+              const uint64_t dah = (second ? dah1 : dah0) + adv_a;
+              const uint64_t dal = (second ? dal1 : dal0) + adv_a;
+              const uint32_t accum = (cb > 0 || kb > 0 || k > 0) ? 1u : 0u;
               if (THREE_X && !C_::CONCAT) {
-                mma_tf32_2sm_warp(d, dal + adv, dbx + adv, idesc, accum);
-                mma_tf32_2sm_warp(d, dah + adv, dbl + adv, idesc, 1u);
-                mma_tf32_2sm_warp(d, dah + adv, dbx + adv, idesc, 1u);
+                mma_tf32_2sm_warp(d, dal, dbx + adv, idesc, accum);
+                mma_tf32_2sm_warp(d, dah, dbl + adv, idesc, 1u);
+                mma_tf32_2sm_warp(d, dah, dbx + adv, idesc, 1u);
               } else if (C_::CONCAT) {
                 // cols [0,BN) += hi*B_hi, cols [BN,2BN) += hi*B_lo   (A_hi read once for both products)
-                mma_tf32_2sm_warp(d, dah + adv, dbz + adv, idesc2, accum);
+                mma_tf32_2sm_warp(d, dah, dbz + adv, idesc2, accum);
                 // cols [0,BN) += lo*B_hi
-                mma_tf32_2sm_warp(d, dal + adv, dbx + adv, idesc, 1u);
+                mma_tf32_2sm_warp(d, dal, dbx + adv, idesc, 1u);
               } else {
-                mma_tf32_2sm_warp(d, dah + adv, dbx + adv, idesc, accum);
+                mma_tf32_2sm_warp(d, dah, dbx + adv, idesc, accum);
               }
             }
-            mma_commit_2sm_mc_warp(&b_empty[s], 0x3);
+            if (!C_::BRES) mma_commit_2sm_mc_warp(&b_empty[s], 0x3);
           }
           mma_commit_2sm_mc_warp(&h_empty[h], 0x3);
         }
@@ -244,11 +325,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     for (int tt = cid; tt < args.total; tt += ncl) {
       for (int cb = 0; cb < args.ncb; ++cb, ++hit) {
         const int h = hit % HS;
+        if (GEOM == GS2D && args.raw) {
+          // build the s2d halo: pixel p = (hi, wi) of the 19 x 16 halo, 16-byte chunk k = slots 4k..4k+3,
+          // slot = (b*2 + d)*C + c <- raw[2*hi + b][2*wi + d][c]; SWIZZLE_64B placement (chunk k of the
+          // 64-byte pixel row goes to k ^ ((p >> 1) & 3)), as the TMA would have written X'
+          mbar_wait(raw_ld, hit & 1);
+          const HTile tl = hdecode(args, tt, rank);
+          const int C = args.rc, rowf = raw_row_floats(C);
+          const int shift = ((2 * tl.wo0 - args.rpl) * C) & 3;  // patch origin within the aligned load
+          const uint32_t rb = smem_u32(raw), hh = smem_u32(halo_hi(h)), hl = smem_u32(halo_lo(h));
+          // thread t always handles chunk k = t & 3 of pixels p = (t >> 2) + 32 j: column wc and the swizzle
+          // phase are fixed, the halo row advances by 2 per step -- all index math hoisted
+          const int k = t & 3, p0 = t >> 2;
+          const int wc = p0 % HWD;
+          int soff[4];  // raw float offset of slot 4k+e relative to (2*hr rows, 2*wc pixels), -1 = zero
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int slot = 4 * k + e;
+            const int bd = slot / C, c = slot - bd * C;
+            soff[e] = bd < 4 ? (bd >> 1) * rowf + shift + (2 * wc + (bd & 1)) * C + c : -1;
+          }
+          const uint32_t chunk_off = (uint32_t)((k ^ ((p0 >> 1) & 3)) << 4);
+          for (int p = p0; p < G_::HALO_ROWS; p += 32) {
+            const int hr = p / HWD;
+            const uint32_t rrow = rb + 4u * (uint32_t)(2 * hr * rowf);
+            float v[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = soff[e] >= 0 ? lds32(rrow + 4u * (uint32_t)soff[e]) : 0.f;
+            const uint32_t off = (uint32_t)(p * 64) + chunk_off;
+            sts128(hh + off, make_float4(v[0], v[1], v[2], v[3]));
+            if (THREE_X)
+              sts128(hl + off, make_float4(v[0] - tf32_hi(v[0]), v[1] - tf32_hi(v[1]), v[2] - tf32_hi(v[2]),
+                                           v[3] - tf32_hi(v[3])));
+          }
+          mbar_arrive(raw_empty);
+          fence_proxy_async_smem();
+          mbar_arrive_remote(h_full_leader + (uint32_t)(h * sizeof(uint64_t)));
+          continue;
+        }
         mbar_wait(&h_ld[h], (hit / HS) & 1);
         if (THREE_X) {
           // elementwise lo = x - trunc_tf32(x) over the whole halo (layout-agnostic: same offsets)
           const uint32_t hi = smem_u32(halo_hi(h)), lo = smem_u32(halo_lo(h));
-          for (int q = t; q < HALO_ROWS * 8; q += 128) {
+          for (int q = t; q < HALO_BYTES / 16; q += 128) {
             const float4 v = lds128(hi + q * 16);
             sts128(lo + q * 16, make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z),
                                              v.w - tf32_hi(v.w)));
@@ -323,21 +442,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     tc_fence_after();
     tmem_dealloc_2sm<C_::TMEM_COLS>(tmem_base);
   }
+  if (threadIdx.x == 0 && args.trace) args.trace[blockIdx.x * 8 + 7] = globaltimer_ns();
 }
 
-template <int BN, bool THREE_X>
+template <int BN, bool THREE_X, int GEOM>
 cudaError_t launch_h(const CUtensorMap& x, const CUtensorMap& bh, const CUtensorMap& bhf, const CUtensorMap& blf,
                      const CUtensorMap& dm, const HArgs& a, int clusters, cudaStream_t s) {
-  using C_ = HCfg<BN, THREE_X>;
-  auto kern = halo_kernel<BN, THREE_X>;
+  using C_ = HCfg<BN, THREE_X, GEOM>;
+  auto kern = halo_kernel<BN, THREE_X, GEOM>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<dim3(2 * clusters), NTHREADS, C_::SMEM, s>>>(x, bh, bhf, blf, dm, a);
-  return cudaGetLastError();
+  return launch_k(kern, dim3(2 * clusters), dim3(NTHREADS), C_::SMEM, s, x, bh, bhf, blf, dm, a);
 }
 
 }  // namespace
@@ -347,12 +466,30 @@ bool halo_ok(const Problem& p) {
          (int64_t)p.N * ((p.HO + TH - 1) / TH) * ((p.WO + TW - 1) / TW) < (1 << 30);
 }
 
-cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_hi, const float* bt_lo, int64_t kpad,
-                             int64_t npad, int block_n, float* out, cudaStream_t s) {
+// Space-to-depth stem (GS2D): a K x K / stride-2 conv with K in {7, 8} and C <= 4 equals a 4x4 /
+// stride-1 VALID conv over X'[n][i][j][(b*2 + d)*C + c] = x[n][2i + b - PT][2j + d - PL][c] (16 channel
+// slots, zero outside the image / past 4C) with W'[a][e][(b*2 + d)*C + c][f] = w[2a + b][2e + d][c][f]
+// (zero past K).  X' is (N, HO + 3, WO + 3, 16).
+bool s2d_ok(const Problem& p) {
+  return p.SH == 2 && p.SW == 2 && (p.KH == 7 || p.KH == 8) && (p.KW == 7 || p.KW == 8) && p.C <= 4 &&
+         p.F <= 128 && (int64_t)p.N * ((p.HO + TH - 1) / TH) * ((p.WO + TW - 1) / TW) < (1 << 30) &&
+         (int64_t)p.N * (p.HO + 3) * (p.WO + 3) * 16 < (1LL << 31);
+}
+
+namespace {
+// Shared host path: tensor maps for the halo boxes (geometry GEOM), B (K-major Bt hi/lo, kpad x npad)
+// and the output, then the launch.  x = the NHWC tensor the halo boxes read (X' for GS2D) with dims
+// (n, h, w, cx).
+template <int GEOM>
+cudaError_t launch_halo_geo(const Problem& p, const float* x, int h, int w, int cx, int pt, int pl, int ncb,
+                            const float* bt_hi, const float* bt_lo, int64_t kpad, int64_t npad, int block_n,
+                            float* out, cudaStream_t s, bool raw = false) {
+  using G_ = Geo<GEOM>;
   const bool three_x = bt_lo != nullptr;
   HArgs a{};
-  a.N = p.N; a.H = p.H; a.W = p.W; a.HO = p.HO; a.WO = p.WO; a.PT = p.pad_top; a.PL = p.pad_left;
-  a.ncb = p.C / 32;
+  a.trace = gemm2_trace_record();
+  a.N = p.N; a.H = h; a.W = w; a.HO = p.HO; a.WO = p.WO; a.PT = pt; a.PL = pl;
+  a.ncb = ncb;
   a.tiles_w = (p.WO + TW - 1) / TW;
   a.tiles_h = (p.HO + TH - 1) / TH;
   a.cta_tiles = p.N * a.tiles_w * a.tiles_h;
@@ -364,11 +501,22 @@ cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_
   a.ldd = p.F;
   a.d = out;
   alignas(64) CUtensorMap tx{}, tbh{}, tbhf{}, tblf{}, td{};
-  {  // input halo boxes: {32 ch, 16 w, 18 h, 1 n} over NHWC, OOB (padding) -> 0
-    const uint64_t dims[4] = {(uint64_t)p.C, (uint64_t)p.W, (uint64_t)p.H, (uint64_t)p.N};
-    const uint64_t st[3] = {(uint64_t)p.C * 4, (uint64_t)p.W * p.C * 4, (uint64_t)p.H * p.W * p.C * 4};
-    const uint32_t box[4] = {32, HWD, HHT, 1};
-    if (!gemm2_encode_tiled(&tx, 4, in, dims, st, box, true)) return cudaErrorInvalidValue;
+  if (raw) {  // GS2D raw mode: patches {32 * C floats, RAW_ROWS rows, 1} of x viewed as (N, H, W*C)
+    a.raw = 1;
+    a.rc = p.C;
+    a.rpt = p.pad_top;
+    a.rpl = p.pad_left;
+    const uint64_t dims[3] = {(uint64_t)p.W * p.C, (uint64_t)p.H, (uint64_t)p.N};
+    const uint64_t st[2] = {(uint64_t)p.W * p.C * 4, (uint64_t)p.H * p.W * p.C * 4};
+    const uint32_t box[3] = {(uint32_t)raw_row_floats(p.C), (uint32_t)RAW_ROWS, 1};
+    if (!gemm2_encode_tiled(&tx, 3, x, dims, st, box, false)) return cudaErrorInvalidValue;
+  } else {  // input halo boxes {32 | 16 ch, 16 w, HHT h, 1 n} over NHWC, OOB (padding) -> 0
+    const uint64_t dims[4] = {(uint64_t)cx, (uint64_t)w, (uint64_t)h, (uint64_t)p.N};
+    const uint64_t st[3] = {(uint64_t)cx * 4, (uint64_t)w * cx * 4, (uint64_t)h * w * cx * 4};
+    const uint32_t box[4] = {(uint32_t)(G_::ROWB / 4), HWD, G_::HHT, 1};
+    if (!gemm2_encode_tiled_sw(&tx, 4, x, dims, st, box,
+                               GEOM == GS2D ? (int)CU_TENSOR_MAP_SWIZZLE_64B : (int)CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
   }
   {
     const uint64_t dims[3] = {(uint64_t)kpad, (uint64_t)npad, 1};
@@ -396,12 +544,110 @@ cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_
   if (!a.tma_store) td = tbh;
   const int clusters = a.total < 74 ? a.total : 74;
   switch (block_n) {
-    case 64: return three_x ? launch_h<64, true>(tx, tbh, tbhf, tblf, td, a, clusters, s)
-                            : launch_h<64, false>(tx, tbh, tbhf, tblf, td, a, clusters, s);
-    case 128: return three_x ? launch_h<128, true>(tx, tbh, tbhf, tblf, td, a, clusters, s)
-                             : launch_h<128, false>(tx, tbh, tbhf, tblf, td, a, clusters, s);
+    case 64: return three_x ? launch_h<64, true, GEOM>(tx, tbh, tbhf, tblf, td, a, clusters, s)
+                            : launch_h<64, false, GEOM>(tx, tbh, tbhf, tblf, td, a, clusters, s);
+    case 128: return three_x ? launch_h<128, true, GEOM>(tx, tbh, tbhf, tblf, td, a, clusters, s)
+                             : launch_h<128, false, GEOM>(tx, tbh, tbhf, tblf, td, a, clusters, s);
   }
   return cudaErrorInvalidValue;
+}
+
+// X' = s2d(x): block row blockIdx.y = one X' row (n, i); four threads per X' pixel, thread q writes
+// slots 4q..4q+3 (one float4) so a warp stores 512 contiguous bytes; no index divisions beyond / 4;
+// C static so the slot -> (b, d, c) map folds
+template <int C>
+__global__ void s2d_input_kernel(const float* __restrict__ x, int N, int H, int W, int PT, int PL, int Hs, int Ws,
+                                 float* __restrict__ xs) {
+  pdl_trigger();
+  pdl_wait();
+  const int row = blockIdx.y + blockIdx.z * 65535;  // n * Hs + i
+  if (row >= N * Hs) return;
+  const int n = row / Hs, i = row - n * Hs;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;  // j * 4 + q
+  if (g >= Ws * 4) return;
+  const int j = g >> 2, qd = g & 3;
+  float v[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int slot = 4 * qd + e;
+    const int bd = slot / C, c = slot % C;
+    const int ih = 2 * i + (bd >> 1) - PT, iw = 2 * j + (bd & 1) - PL;
+    v[e] = (bd < 4 && ih >= 0 && ih < H && iw >= 0 && iw < W) ? __ldg(x + (((int64_t)n * H + ih) * W + iw) * C + c)
+                                                               : 0.f;
+  }
+  reinterpret_cast<float4*>(xs + (int64_t)row * Ws * 16)[g] = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// Bt'[f][k] (npad x 256, K-major), k = (a*4 + e)*16 + (b*2 + d)*C + c  <-  w[2a+b][2e+d][c][f]; 3xTF32: hi/lo
+__global__ void s2d_filter_kernel(const float* __restrict__ w, int KH, int KW, int C, int F, int64_t npad,
+                                  float* __restrict__ bt_hi, float* __restrict__ bt_lo) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t total = npad * 256;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % 256);
+    const int f = (int)(i / 256);
+    const int tap = k / 16, slot = k % 16;
+    const int a = tap / 4, e = tap % 4;
+    const int bd = C > 0 ? slot / C : 0, c = C > 0 ? slot % C : 0;
+    const int r = 2 * a + (bd >> 1), sc = 2 * e + (bd & 1);
+    float v = 0.f;
+    if (bd < 4 && r < KH && sc < KW && f < F) v = w[((int64_t)(r * KW + sc) * C + c) * F + f];
+    const float h = bt_lo ? tf32_hi(v) : v;
+    bt_hi[i] = h;
+    if (bt_lo) bt_lo[i] = v - h;
+  }
+}
+}  // namespace
+
+cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_hi, const float* bt_lo, int64_t kpad,
+                             int64_t npad, int block_n, float* out, cudaStream_t s) {
+  return launch_halo_geo<G3X3>(p, in, p.H, p.W, p.C, p.pad_top, p.pad_left, p.C / 32, bt_hi, bt_lo, kpad, npad,
+                               block_n, out, s);
+}
+
+size_t s2d_workspace(const Problem& p, int block_n, bool three_x) {
+  const int64_t npad = (p.F + block_n - 1) / block_n * block_n;
+  const size_t bt = (size_t)((npad * 256 * 4 + 255) / 256 * 256);
+  const size_t xs = (size_t)(((int64_t)p.N * (p.HO + 3) * (p.WO + 3) * 16 * 4 + 255) / 256 * 256);
+  return bt * (three_x ? 2 : 1) + xs;
+}
+
+cudaError_t launch_gemm_s2d(const Problem& p, const float* in, const float* filt, int block_n, bool three_x,
+                            void* ws, float* out, cudaStream_t s) {
+  const int64_t npad = (p.F + block_n - 1) / block_n * block_n;
+  const size_t bt = (size_t)((npad * 256 * 4 + 255) / 256 * 256);
+  uint8_t* w8 = static_cast<uint8_t*>(ws);
+  float* bt_hi = reinterpret_cast<float*>(w8);
+  w8 += bt;
+  float* bt_lo = nullptr;
+  if (three_x) {
+    bt_lo = reinterpret_cast<float*>(w8);
+    w8 += bt;
+  }
+  float* xs = reinterpret_cast<float*>(w8);
+  const int hs = p.HO + 3, wsd = p.WO + 3;
+  // raw mode (C <= 3, 16-byte input rows): the GEMM builds s2d halos from raw input patches itself
+  const bool raw = p.C <= 3 && ((int64_t)p.W * p.C) % 4 == 0 && getenv("CONV2D_S2D_PREPASS") == nullptr;
+  if (raw) {
+    int64_t fb = (npad * 256 + 255) / 256;
+    cudaError_t e = launch_k(s2d_filter_kernel, dim3((unsigned)fb), dim3(256), 0, s, filt, p.KH, p.KW, p.C, p.F,
+                             npad, bt_hi, bt_lo);
+    if (e != cudaSuccess) return e;
+    return launch_halo_geo<GS2D>(p, in, hs, wsd, 16, 0, 0, 1, bt_hi, bt_lo, 256, npad, block_n, out, s, true);
+  }
+  const int rows = p.N * hs;
+  auto kin = p.C == 1 ? s2d_input_kernel<1> : p.C == 2 ? s2d_input_kernel<2> : p.C == 3 ? s2d_input_kernel<3>
+                                                                                         : s2d_input_kernel<4>;
+  const dim3 grid((unsigned)((wsd * 4 + 255) / 256), (unsigned)(rows < 65535 ? rows : 65535),
+                  (unsigned)((rows + 65534) / 65535));
+  cudaError_t e = launch_k(kin, grid, dim3(256), 0, s, in, p.N, p.H, p.W, p.pad_top, p.pad_left, hs, wsd, xs);
+  if (e != cudaSuccess) return e;
+  int64_t fb = (npad * 256 + 255) / 256;
+  e = launch_k(s2d_filter_kernel, dim3((unsigned)fb), dim3(256), 0, s, filt, p.KH, p.KW, p.C, p.F, npad, bt_hi,
+               bt_lo);
+  if (e != cudaSuccess) return e;
+  return launch_halo_geo<GS2D>(p, xs, hs, wsd, 16, 0, 0, 1, bt_hi, bt_lo, 256, npad, block_n, out, s);
 }
 
 }  // namespace conv2d

@@ -66,6 +66,9 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
   if (is_1x1 && p.C % 4 == 0 && p.C >= 32 && !((variant & 1) && gemm2_im2col_ok(p))) {
     pl.a_mode = A_DENSE;
     pl.cstride = p.C;
+  } else if (!is_1x1 && s2d_ok(p) && !(variant & 1) && getenv("CONV2D_NO_S2D") == nullptr) {
+    pl.a_mode = A_S2D;  // 7x7/8x8 stride-2 stems, C <= 4: space-to-depth + 4x4 halo views (gemm_halo.cu)
+    pl.cstride = p.C;
   } else if (!is_1x1 && halo_ok(p) && !(variant & 1) && getenv("CONV2D_NO_HALO") == nullptr) {
     pl.a_mode = A_HALO;  // 3x3 s1, small N: halo-tile reuse (gemm_halo.cu)
     pl.cstride = p.C;
@@ -75,7 +78,8 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
   } else if (gemm2_rowseg_ok(p)) {
     // small C, narrow windows (the C=3 stems): A_ROWSEG (one overlapping-stride TMA box per kernel
     // row) by default, A_STEM (halo + transform-built rows) as the tunable alternative
-    pl.a_mode = ((variant & 1) && gemm2_stem_ok(p, pl.block_n, pl.three_x)) ? A_STEM : A_ROWSEG;
+    // (for s2d-eligible stems bit 0 selects this path over A_S2D)
+    pl.a_mode = ((variant & 1) && !s2d_ok(p) && gemm2_stem_ok(p, pl.block_n, pl.three_x)) ? A_STEM : A_ROWSEG;
     pl.cg = (int)round_up(p.C, 4);
     pl.pad = true;         // spatial + channel padding pass
     pl.cstride = pl.cg;
@@ -102,6 +106,15 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
       pl.cstride = pl.cg;
     }
   }
+  if (pl.a_mode == A_S2D) {
+    if (pl.block_n == 256) pl.block_n = 128;
+    pl.kpad = 256;
+    pl.npad = round_up(p.F, pl.block_n);
+    pl.splits = 1;
+    pl.b_mn = false;
+    pl.total = s2d_workspace(p, pl.block_n, pl.three_x);
+    return pl;
+  }
   const bool rowk = pl.a_mode == A_ROWSEG || pl.a_mode == A_STEM;  // k = (kernel row, 32 floats)
   if (!rowk) pl.rowstride = p.KW * pl.cstride;
   pl.kpad = rowk ? (int64_t)p.KH * 32 : round_up((int64_t)p.KH * p.KW * pl.cstride, 32);
@@ -123,7 +136,7 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
 
 int igemm_variants(const Problem& p, bool is_1x1, int* masks) {
   const bool alt_a = is_1x1 ? (p.C % 4 == 0 && p.C >= 32 && gemm2_im2col_ok(p))
-                            : ((halo_ok(p) && gemm2_im2col_ok(p)) ||
+                            : ((halo_ok(p) && gemm2_im2col_ok(p)) || (s2d_ok(p) && gemm2_rowseg_ok(p)) ||
                                (gemm2_rowseg_ok(p) && gemm2_stem_ok(p, gemm2_choose_block_n(p.F), p.math == 0)));
   const bool alt_n = gemm2_choose_block_n(p.F) == 256;
   // bit 3 matters only where some A path reads B directly (im2col / dense, F % 32 == 0) in 3xTF32 mode
@@ -158,6 +171,7 @@ size_t igemm_workspace(const Problem& p, bool is_1x1) {
 
 int igemm_launches(const Problem& p, bool is_1x1) {
   const Plan pl = make_plan(p, is_1x1, variant_of(p, is_1x1));
+  if (pl.a_mode == A_S2D) return (p.C <= 3 && ((int64_t)p.W * p.C) % 4 == 0) ? 2 : 3;  // [s2d input,] filter, GEMM
   return (pl.b_mn ? 1 : 2) + (pl.pad ? 1 : 0) + (pl.splits > 1 ? 1 : 0);
 }
 
@@ -165,6 +179,7 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
                          cudaStream_t s) {
   const Plan pl = make_plan(p, is_1x1, variant_of(p, is_1x1));
   static const bool debug = getenv("CONV2D_DEBUG") != nullptr;
+  if (pl.a_mode == A_S2D) return launch_gemm_s2d(p, in, filt, pl.block_n, pl.three_x, ws, out, s);
   if (debug)
     fprintf(stderr, "[conv2d] igemm N=%d H=%d W=%d C=%d F=%d K=%dx%d S=%d: a_mode=%d bn=%d splits=%d kpad=%lld 3x=%d\n",
             p.N, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH, pl.a_mode, pl.block_n, pl.splits, (long long)pl.kpad,

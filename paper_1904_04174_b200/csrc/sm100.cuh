@@ -283,6 +283,11 @@ namespace sm100 {
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+__device__ __forceinline__ float lds32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ float4 lds128(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -373,6 +378,17 @@ __device__ __forceinline__ void tma_store_4d(const void* tmap, uint32_t src, int
 namespace sm100 {
 // SWIZZLE_128B K-major tile whose 8-row groups are `sbo` bytes apart and whose start row sits
 // `phase` rows into the 1024-byte swizzle period (matrix base offset, bits [49,52)).
+// K-major SWIZZLE_64B operand (64-byte rows, 8-row / 512-byte atoms; descriptor layout type 4),
+// SBO = byte stride between 8-row groups
+__device__ __forceinline__ uint64_t umma_desc_sw64_kmajor_sbo(uint32_t smem_addr, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)4u << 61;
+  return d;
+}
 __device__ __forceinline__ uint64_t umma_desc_sw128_kmajor_sbo(uint32_t smem_addr, uint32_t sbo, uint32_t phase) {
   uint64_t d = 0;
   d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);

@@ -12,6 +12,7 @@
 //     the four pixel groups of a warp.
 // Exact fp32 FFMA, (c-chunk, c, kh, kw) accumulation order.
 #include "internal.h"
+#include "launch.cuh"
 
 namespace conv2d {
 namespace {
@@ -23,6 +24,8 @@ __global__ void __launch_bounds__(NTHREADS) tiled_kernel(const float* __restrict
                                                          const float* __restrict__ filt, float* __restrict__ out,
                                                          int H, int W, int C, int F, int KH, int KW, int SH, int SW,
                                                          int HO, int WO, int PT, int PL, int fblocks) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float smem[];
   const int CC = C < CCMAX ? C : CCMAX;
   const int CCP = CC + 1;
@@ -122,9 +125,8 @@ cudaError_t launch_tiled(const Problem& p, const float* in, const float* filt, f
   }
   const int fblocks = (p.F + FB - 1) / FB;
   dim3 grid((p.WO + TW - 1) / TW, (p.HO + TH - 1) / TH, (unsigned)(p.N * fblocks));
-  tiled_kernel<<<grid, NTHREADS, smem, s>>>(in, filt, out, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH, p.SW, p.HO, p.WO,
-                                            p.pad_top, p.pad_left, fblocks);
-  return cudaGetLastError();
+  return launch_k(tiled_kernel, grid, dim3(NTHREADS), smem, s, in, filt, out, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH,
+                  p.SW, p.HO, p.WO, p.pad_top, p.pad_left, fblocks);
 }
 
 }  // namespace conv2d

@@ -19,6 +19,7 @@
 // TF32 mode rounds U and V to TF32 with cvt.rna (reading R16); FP32 mode runs the GEMMs
 // in 3xTF32.
 #include "gemm2sm.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace conv2d {
@@ -35,6 +36,8 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // U_xi stored K-major per xi: Ut[xi][f][c], Fpad rows x Cpad cols.
 __global__ void wino_filter_kernel(const float* __restrict__ w, int C, int F, int64_t cpad, int64_t fpad,
                                    float* __restrict__ ut_hi, float* __restrict__ ut_lo, int mode /*0 3x,1 tf32*/) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = cpad * fpad;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int f = (int)(i % fpad);
@@ -85,6 +88,8 @@ __global__ void wino_filter_kernel(const float* __restrict__ w, int C, int F, in
 // V[xi][t][c] (row stride cpad), t = (n, th, tw)
 __global__ void wino_input_kernel(const float* __restrict__ x, int H, int W, int C, int TH, int TW, int PT, int PL,
                                   int64_t T, int64_t cpad, float* __restrict__ V, int round_rna) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = T * cpad;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % cpad);
@@ -128,6 +133,8 @@ __global__ void wino_input_kernel(const float* __restrict__ x, int H, int W, int
 // Y tile = A^T M A, M[xi][t][f] (row stride ldm)
 __global__ void wino_output_kernel(const float* __restrict__ Mw, int64_t T, int64_t ldm, int F, int HO, int WO,
                                    int TH, int TW, float* __restrict__ y) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = T * F;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int f = (int)(i % F);
@@ -213,13 +220,11 @@ cudaError_t launch_winograd(const Problem& p, const float* in, const float* filt
   b += w.m_bytes;
   float* partial = w.splits > 1 ? reinterpret_cast<float*>(b) : nullptr;
 
-  wino_filter_kernel<<<grid_for(w.cpad * w.fpad), 256, 0, s>>>(filt, p.C, p.F, w.cpad, w.fpad, ut_hi, ut_lo,
-                                                                w.three_x ? 0 : 1);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_k(wino_filter_kernel, dim3(grid_for(w.cpad * w.fpad)), dim3(256), 0, s, filt, p.C, p.F,
+                           w.cpad, w.fpad, ut_hi, ut_lo, w.three_x ? 0 : 1);
   if (e != cudaSuccess) return e;
-  wino_input_kernel<<<grid_for(w.T * w.cpad), 256, 0, s>>>(in, p.H, p.W, p.C, w.TH, w.TW, p.pad_top, p.pad_left,
-                                                           w.T, w.cpad, V, w.three_x ? 0 : 1);
-  e = cudaGetLastError();
+  e = launch_k(wino_input_kernel, dim3(grid_for(w.T * w.cpad)), dim3(256), 0, s, in, p.H, p.W, p.C, w.TH, w.TW,
+               p.pad_top, p.pad_left, w.T, w.cpad, V, w.three_x ? 0 : 1);
   if (e != cudaSuccess) return e;
   Gemm2Args g{};
   g.a_mode = A_DENSE;
@@ -242,8 +247,8 @@ cudaError_t launch_winograd(const Problem& p, const float* in, const float* filt
   g.block_n = w.block_n;
   e = launch_gemm2(p, g, s);
   if (e != cudaSuccess) return e;
-  wino_output_kernel<<<grid_for(w.T * p.F), 256, 0, s>>>(Mw, w.T, w.ldm, p.F, p.HO, p.WO, w.TH, w.TW, out);
-  return cudaGetLastError();
+  return launch_k(wino_output_kernel, dim3(grid_for(w.T * p.F)), dim3(256), 0, s, Mw, w.T, w.ldm, p.F, p.HO, p.WO,
+                  w.TH, w.TW, out);
 }
 
 }  // namespace conv2d

@@ -128,6 +128,13 @@ EDGE = [
     (2, 10, 10, 48, 64, 1, 1, 1, 1, 0),
     (1, 6, 40, 64, 288, 1, 1, 1, 1, 0),
     (1, 15, 13, 128, 160, 3, 3, 2, 2, 0),
+    # space-to-depth stem path (K in {7, 8}, stride 2, C <= 4, F <= 128): ragged 8x16 output tiles,
+    # odd image sizes, SAME corners, VALID, C = 1 / 2 / 4, K = 8, F not a multiple of 32
+    (1, 37, 29, 3, 64, 7, 7, 2, 2, 0),
+    (2, 40, 36, 1, 32, 7, 7, 2, 2, 1),
+    (1, 33, 47, 2, 100, 8, 8, 2, 2, 0),
+    (3, 20, 18, 4, 128, 7, 7, 2, 2, 0),
+    (1, 64, 64, 3, 64, 8, 7, 2, 2, 1),
 ]
 
 
