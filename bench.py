@@ -418,13 +418,13 @@ def main():
             tj = json.load(fh)
         if tj.get("gemm_launches"):
             traffic = round(tj["gemm_dram_bytes"] / tj["gemm_launches"] / 1e6, 2)
-            traffic_src = (f"MB per gemm2sm launch, ncu dram__bytes_read.sum+write.sum over one timed step "
-                           f"({tj['gemm_launches']} launches; profiles/round1_ncu.md)")
+            traffic_src = (f"MB per GEMM-core launch (gemm2sm / halo), ncu dram__bytes_read.sum+write.sum over one "
+                           f"timed step ({tj['gemm_launches']} launches; profiles/round1_ncu.md)")
     roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(useful_peak, 1), "unit": "TFLOP/s",
             "frac": round(ach / useful_peak, 4), "traffic": traffic,
             "traffic_unit": traffic_src, "algorithmic_mb_per_launch": round(g_bytes / len(grp) / 1e6, 2),
-            "kernel": f"gemm2sm_kernel (persistent 2-CTA tcgen05 GEMM) via conv2d_forward[implicit_gemm|matmul_1x1|"
-                      f"winograd]: {len(grp)} of {len(convs)} convs, {100 * share:.1f}% of step",
+            "kernel": f"GEMM core (persistent 2-CTA tcgen05 kernels gemm2sm / halo) via conv2d_forward[implicit_gemm|"
+                      f"matmul_1x1|winograd]: {len(grp)} of {len(convs)} convs, {100 * share:.1f}% of step",
             "timing": "CUDA events at the timed steps' boundaries (launching stream) x the group's share of "
                       "per-conv event times from K instrumented replays after the timed region",
             "peak_source": f"{peak_src} bf16 burst {peaks['bf16_tflops']} TF/s /2 (TF32)"

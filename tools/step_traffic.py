@@ -1,0 +1,41 @@
+#!/usr/bin/env python
+"""Per-launch DRAM traffic of the GEMM kernels in one timed bench.py step, from an ncu launch list
+taken with --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum over the
+NVTX range "bench_timed" (one step).  Writes the JSON bench.py's roofline.traffic reads.
+
+    python tools/step_traffic.py gpurun_out/launches.csv > profiles/round1_step_traffic.json
+"""
+import csv
+import json
+import re
+import sys
+from collections import defaultdict
+
+GEMM = re.compile(r"gemm2sm_kernel|halo_kernel")
+
+
+def main():
+    path = sys.argv[1]
+    with open(path) as f:
+        lines = [l for l in f if l.startswith('"')]
+    per = defaultdict(dict)
+    names = {}
+    for r in csv.DictReader(lines):
+        per[r["ID"]][r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+        names[r["ID"]] = r["Kernel Name"]
+    n = 0
+    us = total = byts = 0.0
+    for i, m in per.items():
+        t = m.get("gpu__time_duration.sum", 0.0) / 1e3  # ns -> us
+        total += t
+        if GEMM.search(names[i]):
+            n += 1
+            us += t
+            byts += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
+    json.dump({"source": path, "gemm_launches": n, "gemm_us": us, "gemm_dram_bytes": byts, "total_us": total},
+              sys.stdout, indent=1)
+    print()
+
+
+if __name__ == "__main__":
+    main()
