@@ -243,6 +243,8 @@ def main():
     ap.add_argument("--global-batch", type=int, default=GLOBAL_BATCH,
                     help="analysis only (default = BASELINE config 5's 256)")
     ap.add_argument("--layers-out", default="", help="write the per-layer table (JSON) here")
+    ap.add_argument("--save-selection", default="", help="write the tuned selector table here (rank 0)")
+    ap.add_argument("--load-selection", default="", help="seed the selector from this table instead of tuning")
     ap.add_argument("--trace-out", default="", help="diagnostics: per-launch GEMM timeline of one extra "
                     "(untimed) graph replay of the step, JSON (include/conv2d_debug.h)")
     args = ap.parse_args()
@@ -296,10 +298,16 @@ def main():
     # ---- auto-selection (measured, once per distinct layer); rank 0's choices broadcast so every
     #      rank runs the same kernels (off the timed path)
     chosen = {}
+    if args.load_selection:
+        C.conv2d_load_selection(args.load_selection)
     for cv in convs:
         key = cv["layer"].name
         if key not in chosen:
-            chosen[key] = C.conv2d_autotune(cv["p"], cv["x"], cv["w"], cv["y"], ws, ws.numel())
+            sel = C.conv2d_selected(cv["p"]) if args.load_selection else None
+            chosen[key] = sel if sel is not None else C.conv2d_autotune(cv["p"], cv["x"], cv["w"], cv["y"], ws,
+                                                                        ws.numel())
+    if args.save_selection and rank == 0:
+        C.conv2d_save_selection(args.save_selection)
     chosen = broadcast_choices(chosen, dist if world > 1 else None, dev)
     for cv in convs:
         C.conv2d_set_selected(cv["p"], chosen[cv["layer"].name])

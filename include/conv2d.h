@@ -79,7 +79,8 @@ typedef enum {
   CONV2D_ERR_ALIGNMENT = 4,      /* a device pointer is not 16-byte aligned */
   CONV2D_ERR_NULL = 5,           /* a required pointer argument is NULL */
   CONV2D_ERR_CUDA = 6,           /* a CUDA call failed; see conv2d_last_error() */
-  CONV2D_ERR_NO_DEVICE = 7       /* no sm_100 device is current */
+  CONV2D_ERR_NO_DEVICE = 7,      /* no sm_100 device is current */
+  CONV2D_ERR_IO = 8              /* selection-table file could not be opened / written */
 } conv2d_status_t;
 
 /* Shape inference (no device needed).  out_nhwf = {N, Ho, Wo, F};
@@ -125,6 +126,20 @@ conv2d_status_t conv2d_set_selected(const conv2d_params_t* p, conv2d_algo_t algo
 
 /* Drop every cached choice. */
 void conv2d_clear_selection_cache(void);
+
+/* Persisted selector table ("table serialization round-trips", SPEC.md:354's line format with
+ * this library's full cache key).  One line per cached choice of the current device:
+ *     N H W C F KH KW SH SW same|valid fp32|tf32 : algorithm[/variant]
+ * (variant = the tuned algorithm parameters of implicit_gemm / matmul_1x1, see igemm.cu), then
+ * `default : a,b,...` (algorithms by number of entries won; informative) and `#` comments.
+ * save: CONV2D_ERR_IO if the file cannot be written.  load: parses and validates every line first
+ * (CONV2D_ERR_INVALID_PARAMS for malformed lines / unknown names / invalid params,
+ * CONV2D_ERR_UNSUPPORTED if an algorithm cannot run its params -- detail with file:line in
+ * conv2d_last_error()); only a fully valid file is applied, seeding the cache (and variants) so
+ * conv2d_forward(AUTO) uses the stored choices without tuning.  *loaded = entries applied (may be NULL).
+ * Host-only: neither touches device memory. */
+conv2d_status_t conv2d_save_selection(const char* path);
+conv2d_status_t conv2d_load_selection(const char* path, int* loaded);
 
 /* Last per-algorithm best times (microseconds) from the most recent autotune on
  * this thread; times[a] < 0 for algorithms not timed.  times must hold CONV2D_NUM_ALGOS. */

@@ -31,14 +31,15 @@ ALGO_NAMES = ["auto", "direct", "tiled", "implicit_gemm", "winograd_f2x2_3x3", "
 ALGO_BY_NAME = {n: i for i, n in enumerate(ALGO_NAMES)}
 
 STATUS = ["CONV2D_OK", "CONV2D_ERR_INVALID_PARAMS", "CONV2D_ERR_UNSUPPORTED", "CONV2D_ERR_WORKSPACE",
-          "CONV2D_ERR_ALIGNMENT", "CONV2D_ERR_NULL", "CONV2D_ERR_CUDA", "CONV2D_ERR_NO_DEVICE"]
-OK, ERR_INVALID_PARAMS, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_ALIGNMENT, ERR_NULL, ERR_CUDA, ERR_NO_DEVICE = range(8)
+          "CONV2D_ERR_ALIGNMENT", "CONV2D_ERR_NULL", "CONV2D_ERR_CUDA", "CONV2D_ERR_NO_DEVICE",
+                "CONV2D_ERR_IO"]
+OK, ERR_INVALID_PARAMS, ERR_UNSUPPORTED, ERR_WORKSPACE, ERR_ALIGNMENT, ERR_NULL, ERR_CUDA, ERR_NO_DEVICE, ERR_IO = range(9)
 
 EXPORTED = ["conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv2d_query_workspace",
             "conv2d_forward", "conv2d_autotune", "conv2d_selected", "conv2d_set_selected",
             "conv2d_clear_selection_cache", "conv2d_last_tune_times", "conv2d_launch_count",
             "conv2d_synth_fill", "conv2d_status_string", "conv2d_algo_name", "conv2d_last_error",
-            "conv2d_debug_trace"]
+            "conv2d_debug_trace", "conv2d_save_selection", "conv2d_load_selection"]
 
 
 class conv2d_params_t(ctypes.Structure):
@@ -76,6 +77,8 @@ _lib.conv2d_algo_name.argtypes = [ctypes.c_int]
 _lib.conv2d_algo_name.restype = ctypes.c_char_p
 _lib.conv2d_last_error.argtypes = []
 _lib.conv2d_debug_trace.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+_lib.conv2d_save_selection.argtypes = [ctypes.c_char_p]
+_lib.conv2d_load_selection.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int)]
 _lib.conv2d_debug_trace.restype = ctypes.c_int
 _lib.conv2d_last_error.restype = ctypes.c_char_p
 for _f in ("conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv2d_query_workspace",
@@ -208,6 +211,16 @@ def conv2d_status_string(s: int) -> str:
 
 def conv2d_last_error() -> str:
     return _lib.conv2d_last_error().decode()
+
+
+def conv2d_save_selection(path: str) -> None:
+    _check(_lib.conv2d_save_selection(str(path).encode()), "conv2d_save_selection")
+
+
+def conv2d_load_selection(path: str) -> int:
+    n = ctypes.c_int(0)
+    _check(_lib.conv2d_load_selection(str(path).encode(), ctypes.byref(n)), "conv2d_load_selection")
+    return n.value
 
 
 def conv2d_debug_trace(enable: int, read: bool = False) -> list:

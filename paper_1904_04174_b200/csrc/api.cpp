@@ -16,6 +16,9 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <vector>
+#include <cctype>
+#include <cstdlib>
 
 #include "internal.h"
 #include "../../include/conv2d_debug.h"
@@ -391,6 +394,189 @@ conv2d_status_t conv2d_set_selected(const conv2d_params_t* p, conv2d_algo_t algo
   return CONV2D_OK;
 }
 
+// ---- persisted selector table (SPEC.md:354's line format, with the full key of this library's cache)
+//   N H W C F KH KW SH SW same|valid fp32|tf32 : algo[/variant]
+//   default : algo,algo,...        (ranking by win count over the entries; informative)
+conv2d_status_t conv2d_save_selection(const char* path) {
+  if (!path) return fail(CONV2D_ERR_NULL, "path is NULL");
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  std::vector<std::pair<Key, conv2d_algo_t>> rows;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (const auto& kv : g_cache)
+      if (std::get<11>(kv.first) == dev) rows.push_back(kv);
+  }
+  FILE* f = fopen(path, "w");
+  if (!f) return fail(CONV2D_ERR_IO, std::string("cannot open for writing: ") + path);
+  fprintf(f, "# conv2d selection table v1: N H W C F KH KW SH SW padding math : algorithm[/variant]\n");
+  int wins[CONV2D_NUM_ALGOS] = {0};
+  for (const auto& kv : rows) {
+    const Key& k = kv.first;
+    conv2d_params_t p{std::get<0>(k), std::get<1>(k), std::get<2>(k), std::get<3>(k), std::get<4>(k), std::get<5>(k),
+                      std::get<6>(k), std::get<7>(k), std::get<8>(k), (conv2d_padding_t)std::get<9>(k),
+                      (conv2d_math_t)std::get<10>(k)};
+    fprintf(f, "%d %d %d %d %d %d %d %d %d %s %s : %s", p.batch, p.in_rows, p.in_cols, p.channels, p.features,
+            p.window_rows, p.window_cols, p.stride_rows, p.stride_cols, p.padding == CONV2D_PAD_SAME ? "same" : "valid",
+            p.math == CONV2D_MATH_FP32 ? "fp32" : "tf32", conv2d_algo_name(kv.second));
+    Problem q;
+    std::string why;
+    int v = 0;
+    if ((kv.second == CONV2D_ALGO_IMPLICIT_GEMM || kv.second == CONV2D_ALGO_MATMUL_1X1) && shape_of(&p, &q, &why) &&
+        igemm_get_variant(q, kv.second == CONV2D_ALGO_MATMUL_1X1, &v))
+      fprintf(f, "/%d", v);
+    fprintf(f, "\n");
+    ++wins[kv.second];
+  }
+  fprintf(f, "default :");
+  bool used[CONV2D_NUM_ALGOS] = {false};
+  for (int n = 0, first = 1; n < CONV2D_NUM_ALGOS - 1; ++n) {
+    int best = -1;
+    for (int a = 1; a < CONV2D_NUM_ALGOS; ++a)  // most wins first, ties in enum order
+      if (!used[a] && (best < 0 || wins[a] > wins[best])) best = a;
+    used[best] = true;
+    fprintf(f, "%s%s", first ? " " : ",", conv2d_algo_name((conv2d_algo_t)best));
+    first = 0;
+  }
+  fprintf(f, "\n");
+  const bool ok = fclose(f) == 0;
+  return ok ? CONV2D_OK : fail(CONV2D_ERR_IO, std::string("write failed: ") + path);
+}
+
+conv2d_status_t conv2d_load_selection(const char* path, int* loaded) {
+  if (!path) return fail(CONV2D_ERR_NULL, "path is NULL");
+  if (loaded) *loaded = 0;
+  FILE* f = fopen(path, "r");
+  if (!f) return fail(CONV2D_ERR_IO, std::string("cannot open: ") + path);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  struct Entry {
+    conv2d_params_t p;
+    conv2d_algo_t a;
+    int variant;
+  };
+  std::vector<Entry> entries;
+  char line[512];
+  int lineno = 0;
+  conv2d_status_t st = CONV2D_OK;
+  std::string why;
+  auto algo_by_name = [](const std::string& n) -> int {
+    for (int a = 1; a < CONV2D_NUM_ALGOS; ++a)
+      if (n == conv2d_algo_name((conv2d_algo_t)a)) return a;
+    return -1;
+  };
+  while (st == CONV2D_OK && fgets(line, sizeof line, f)) {
+    ++lineno;
+    std::string l(line);
+    const size_t hash = l.find('#');
+    if (hash != std::string::npos) l.erase(hash);
+    while (!l.empty() && isspace((unsigned char)l.back())) l.pop_back();
+    size_t b = 0;
+    while (b < l.size() && isspace((unsigned char)l[b])) ++b;
+    l.erase(0, b);
+    if (l.empty()) continue;
+    const size_t colon = l.find(':');
+    if (colon == std::string::npos) {
+      st = CONV2D_ERR_INVALID_PARAMS;
+      why = "missing ':'";
+      break;
+    }
+    std::string lhs = l.substr(0, colon), rhs = l.substr(colon + 1);
+    while (!rhs.empty() && isspace((unsigned char)rhs.front())) rhs.erase(0, 1);
+    while (!lhs.empty() && isspace((unsigned char)lhs.back())) lhs.pop_back();
+    if (lhs == "default") {  // validate the ranking; it is informative only
+      size_t pos = 0;
+      while (pos <= rhs.size()) {
+        const size_t c = rhs.find(',', pos);
+        std::string n = rhs.substr(pos, c == std::string::npos ? std::string::npos : c - pos);
+        while (!n.empty() && isspace((unsigned char)n.back())) n.pop_back();
+        while (!n.empty() && isspace((unsigned char)n.front())) n.erase(0, 1);
+        if (algo_by_name(n) < 0) {
+          st = CONV2D_ERR_INVALID_PARAMS;
+          why = "unknown algorithm '" + n + "' in default ranking";
+          break;
+        }
+        if (c == std::string::npos) break;
+        pos = c + 1;
+      }
+      continue;
+    }
+    Entry e{};
+    char pad[16] = {0}, math[16] = {0};
+    int extra = 0;
+    const int got = sscanf(lhs.c_str(), "%d %d %d %d %d %d %d %d %d %15s %15s %n", &e.p.batch, &e.p.in_rows,
+                           &e.p.in_cols, &e.p.channels, &e.p.features, &e.p.window_rows, &e.p.window_cols,
+                           &e.p.stride_rows, &e.p.stride_cols, pad, math, &extra);
+    if (got != 11 || (size_t)extra != lhs.size()) {
+      st = CONV2D_ERR_INVALID_PARAMS;
+      why = "expected 'N H W C F KH KW SH SW padding math'";
+      break;
+    }
+    const std::string ps(pad), ms(math);
+    if ((ps != "same" && ps != "valid") || (ms != "fp32" && ms != "tf32")) {
+      st = CONV2D_ERR_INVALID_PARAMS;
+      why = "padding must be same|valid and math fp32|tf32";
+      break;
+    }
+    e.p.padding = ps == "same" ? CONV2D_PAD_SAME : CONV2D_PAD_VALID;
+    e.p.math = ms == "fp32" ? CONV2D_MATH_FP32 : CONV2D_MATH_TF32;
+    e.variant = -1;
+    std::string an = rhs;
+    const size_t slash = rhs.find('/');
+    if (slash != std::string::npos) {
+      an = rhs.substr(0, slash);
+      char* end = nullptr;
+      const long v = strtol(rhs.c_str() + slash + 1, &end, 10);
+      if (!end || *end != '\0' || v < 0 || v > 15) {
+        st = CONV2D_ERR_INVALID_PARAMS;
+        why = "bad variant";
+        break;
+      }
+      e.variant = (int)v;
+    }
+    const int a = algo_by_name(an);
+    if (a < 0) {
+      st = CONV2D_ERR_INVALID_PARAMS;
+      why = "unknown algorithm '" + an + "'";
+      break;
+    }
+    e.a = (conv2d_algo_t)a;
+    Problem q;
+    std::string w;
+    if (!shape_of(&e.p, &q, &w)) {
+      st = CONV2D_ERR_INVALID_PARAMS;
+      why = w;
+      break;
+    }
+    if (!algo_supports(q, e.a)) {
+      st = CONV2D_ERR_UNSUPPORTED;
+      why = std::string(conv2d_algo_name(e.a)) + " does not support these params";
+      break;
+    }
+    if (e.variant >= 0 && e.a != CONV2D_ALGO_IMPLICIT_GEMM && e.a != CONV2D_ALGO_MATMUL_1X1) {
+      st = CONV2D_ERR_INVALID_PARAMS;
+      why = "a variant is only defined for implicit_gemm / matmul_1x1";
+      break;
+    }
+    entries.push_back(e);
+  }
+  fclose(f);
+  if (st != CONV2D_OK) return fail(st, std::string(path) + ":" + std::to_string(lineno) + ": " + why);
+  {  // all lines valid: apply (an invalid file leaves the cache untouched)
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    for (const auto& e : entries) g_cache[key_of(&e.p, dev)] = e.a;
+  }
+  for (const auto& e : entries)
+    if (e.variant >= 0) {
+      Problem q;
+      std::string w;
+      shape_of(&e.p, &q, &w);
+      igemm_set_variant(q, e.a == CONV2D_ALGO_MATMUL_1X1, e.variant);
+    }
+  if (loaded) *loaded = (int)entries.size();
+  return CONV2D_OK;
+}
+
 void conv2d_clear_selection_cache(void) {
   std::lock_guard<std::mutex> lk(g_cache_mu);
   g_cache.clear();
@@ -434,6 +620,7 @@ const char* conv2d_status_string(conv2d_status_t s) {
     case CONV2D_ERR_NULL: return "CONV2D_ERR_NULL";
     case CONV2D_ERR_CUDA: return "CONV2D_ERR_CUDA";
     case CONV2D_ERR_NO_DEVICE: return "CONV2D_ERR_NO_DEVICE";
+    case CONV2D_ERR_IO: return "CONV2D_ERR_IO";
   }
   return "CONV2D_ERR_UNKNOWN";
 }

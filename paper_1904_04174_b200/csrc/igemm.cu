@@ -156,6 +156,14 @@ int igemm_variants(const Problem& p, bool is_1x1, int* masks) {
   return n;
 }
 
+bool igemm_get_variant(const Problem& p, bool is_1x1, int* v) {
+  std::lock_guard<std::mutex> lk(g_vmu);
+  auto it = g_variant.find(vkey(p, is_1x1));
+  if (it == g_variant.end()) return false;
+  *v = it->second;
+  return true;
+}
+
 void igemm_set_variant(const Problem& p, bool is_1x1, int v) {
   std::lock_guard<std::mutex> lk(g_vmu);
   g_variant[vkey(p, is_1x1)] = v;

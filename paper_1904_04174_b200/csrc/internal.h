@@ -32,6 +32,7 @@ cudaError_t launch_tiled(const Problem& p, const float* in, const float* filt, f
 size_t igemm_workspace(const Problem& p, bool is_1x1);  // max over variants
 int igemm_variants(const Problem& p, bool is_1x1, int* masks);  // tunable parameter masks (<= 8)
 void igemm_set_variant(const Problem& p, bool is_1x1, int v);
+bool igemm_get_variant(const Problem& p, bool is_1x1, int* v);  // false if never set
 int igemm_launches(const Problem& p, bool is_1x1);
 cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const float* filt, float* out, void* ws,
                          cudaStream_t s);

@@ -251,3 +251,24 @@ def test_algorithm_parameter_variants(cuda_ok, monkeypatch, variant, case):
                 continue
             check_close(p, gpu_conv(p, x, w, a), ref, den, a, f"variant {variant} {case} {math} {a}")
             assert np.array_equal(gpu_conv(p, xi, wi, a), refi)
+
+
+def test_selection_table_gpu_round_trip(cuda_ok, tmp_path):
+    """N4: the tuned choice (algorithm + its parameter variant) survives save -> clear -> load, and
+    conv2d_forward(AUTO) then runs the loaded choice without tuning (same bits)."""
+    c = C()
+    p = P(8, 28, 28, 128, 512, 1, 1, 1, 1, 0)
+    x, w = make_inputs(p, layer_id=1000)
+    c.conv2d_clear_selection_cache()
+    y0 = gpu_conv(p, x, w, c.ALGO_AUTO)
+    a0 = c.conv2d_selected(p)
+    f = tmp_path / "sel.txt"
+    c.conv2d_save_selection(str(f))
+    text = f.read_text()
+    assert f": {c.conv2d_algo_name(a0)}" in text
+    c.conv2d_clear_selection_cache()
+    assert c.conv2d_selected(p) is None
+    assert c.conv2d_load_selection(str(f)) >= 1
+    assert c.conv2d_selected(p) == a0
+    y1 = gpu_conv(p, x, w, c.ALGO_AUTO)
+    assert np.array_equal(y0, y1)
