@@ -26,7 +26,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
-_SRC = [os.path.join(_HERE, "oracle.c")]
+_SRC = [os.path.join(_HERE, "oracle.c"), os.path.join(_HERE, "pool.c")]
 
 SAME, VALID = 0, 1
 
@@ -66,6 +66,34 @@ class Params:
                        self.padding)
 
 
+POOL_MAX, POOL_AVG = 0, 1
+
+
+class _PoolParams(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "batch", "in_rows", "in_cols", "channels", "window_rows", "window_cols", "stride_rows",
+        "stride_cols", "padding", "op")]
+
+
+@dataclass(frozen=True)
+class PoolParams:
+    """NHWC pooling (pool.c): op POOL_MAX / POOL_AVG, padding SAME / VALID."""
+    batch: int
+    in_rows: int
+    in_cols: int
+    channels: int
+    window_rows: int
+    window_cols: int
+    stride_rows: int = 1
+    stride_cols: int = 1
+    padding: int = SAME
+    op: int = POOL_MAX
+
+    def c(self) -> _PoolParams:
+        return _PoolParams(self.batch, self.in_rows, self.in_cols, self.channels, self.window_rows,
+                           self.window_cols, self.stride_rows, self.stride_cols, self.padding, self.op)
+
+
 _lib = None
 
 
@@ -89,6 +117,11 @@ def _load():
         lib.oracle_conv2d_point.restype = ctypes.c_int
         lib.oracle_conv2d_points.argtypes = [P, fp, fp, i64p, ctypes.c_int64, dp, dp, ctypes.c_int]
         lib.oracle_conv2d_points.restype = ctypes.c_int
+        PP = ctypes.POINTER(_PoolParams)
+        lib.oracle_pool2d_shape.argtypes = [PP, i32p, i32p]
+        lib.oracle_pool2d_shape.restype = ctypes.c_int
+        lib.oracle_pool2d.argtypes = [PP, fp, fp, ctypes.c_int]
+        lib.oracle_pool2d.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -173,3 +206,27 @@ def normalized_error(y: np.ndarray, y_ref: np.ndarray, denom: np.ndarray) -> flo
         return 0.0
     ratio = np.where(zero, 0.0, err / np.where(zero, 1.0, denom))
     return float(ratio.max())
+
+
+def pool_output_shape(p: PoolParams):
+    """((N, Ho, Wo, C), (pad_top, pad_bottom, pad_left, pad_right)); ValueError if invalid."""
+    o = (ctypes.c_int32 * 4)()
+    pd = (ctypes.c_int32 * 4)()
+    if _load().oracle_pool2d_shape(ctypes.byref(p.c()), o, pd):
+        raise ValueError(f"invalid pool params {p}")
+    return tuple(o), tuple(pd)
+
+
+def pool2d(p: PoolParams, x: np.ndarray, threads: int | None = None) -> np.ndarray:
+    """Oracle pooling of an NHWC fp32 tensor -> fp32 (N, Ho, Wo, C)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    if x.shape != (p.batch, p.in_rows, p.in_cols, p.channels):
+        raise ValueError(f"input shape {x.shape} != NHWC {(p.batch, p.in_rows, p.in_cols, p.channels)}")
+    shp, _ = pool_output_shape(p)
+    y = np.empty(shp, dtype=np.float32)
+    if threads is None:
+        threads = os.cpu_count() or 1
+    st = _load().oracle_pool2d(ctypes.byref(p.c()), _fptr(x), _fptr(y), threads)
+    if st:
+        raise ValueError(f"oracle_pool2d failed ({st})")
+    return y

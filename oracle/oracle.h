@@ -69,6 +69,24 @@ int oracle_conv2d_point(const oracle_params* p, const float* in, const float* fi
 int oracle_conv2d_points(const oracle_params* p, const float* in, const float* filt,
                          const int64_t* idx, int64_t count, double* y, double* denom, int threads);
 
+/* ---- pooling (pool.c) -------------------------------
+ * NHWC max / average pooling.  The window of output (n, ho, wo, c) is the in-bounds subset of
+ * {(ho*Sr + kh - pad_top, wo*Sc + kw - pad_left)}; max = its maximum, avg = its double sum / its
+ * count, rounded once.  Shapes: the convolution's (features := channels). */
+enum { ORACLE_POOL_MAX = 0, ORACLE_POOL_AVG = 1 };
+
+typedef struct {
+  int32_t batch, in_rows, in_cols, channels;
+  int32_t window_rows, window_cols, stride_rows, stride_cols;
+  int32_t padding; /* ORACLE_SAME / ORACLE_VALID */
+  int32_t op;      /* ORACLE_POOL_MAX / ORACLE_POOL_AVG */
+} oracle_pool_params;
+
+/* 0 and {N, Ho, Wo, C}, {top, bottom, left, right}; 1 on invalid params. */
+int oracle_pool2d_shape(const oracle_pool_params* p, int32_t out_nhwc[4], int32_t pads_tblr[4]);
+/* 0 on success, 1 invalid params, 2 if some window had no in-bounds element. */
+int oracle_pool2d(const oracle_pool_params* p, const float* in, float* out, int threads);
+
 #ifdef __cplusplus
 }
 #endif
