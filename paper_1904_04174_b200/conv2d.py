@@ -39,7 +39,8 @@ EXPORTED = ["conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv
             "conv2d_forward", "conv2d_autotune", "conv2d_selected", "conv2d_set_selected",
             "conv2d_clear_selection_cache", "conv2d_last_tune_times", "conv2d_launch_count",
             "conv2d_synth_fill", "conv2d_status_string", "conv2d_algo_name", "conv2d_last_error",
-            "conv2d_debug_trace", "conv2d_save_selection", "conv2d_load_selection"]
+            "conv2d_debug_trace", "conv2d_save_selection", "conv2d_load_selection",
+            "pool2d_output_shape", "pool2d_forward"]
 
 
 class conv2d_params_t(ctypes.Structure):
@@ -81,7 +82,19 @@ _lib.conv2d_save_selection.argtypes = [ctypes.c_char_p]
 _lib.conv2d_load_selection.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int)]
 _lib.conv2d_debug_trace.restype = ctypes.c_int
 _lib.conv2d_last_error.restype = ctypes.c_char_p
-for _f in ("conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv2d_query_workspace",
+POOL_MAX, POOL_AVG = 0, 1
+
+
+class pool2d_params_t(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "batch", "in_rows", "in_cols", "channels", "window_rows", "window_cols", "stride_rows", "stride_cols",
+        "padding", "op")]
+
+
+_PP = ctypes.POINTER(pool2d_params_t)
+_lib.pool2d_output_shape.argtypes = [_PP, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+_lib.pool2d_forward.argtypes = [_PP, _vp, _vp, _vp]
+for _f in ("pool2d_output_shape", "pool2d_forward", "conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv2d_query_workspace",
            "conv2d_forward", "conv2d_autotune", "conv2d_selected", "conv2d_set_selected",
            "conv2d_launch_count", "conv2d_synth_fill"):
     getattr(_lib, _f).restype = ctypes.c_int
@@ -110,6 +123,37 @@ class Params:
         d = self.__dict__.copy()
         d.update(kw)
         return Params(**d)
+
+
+@dataclass(frozen=True)
+class PoolParams:
+    """include/pool2d.h pool2d_params_t: NHWC max (POOL_MAX) / average (POOL_AVG) pooling."""
+    batch: int
+    in_rows: int
+    in_cols: int
+    channels: int
+    window_rows: int
+    window_cols: int
+    stride_rows: int = 1
+    stride_cols: int = 1
+    padding: int = PAD_SAME
+    op: int = POOL_MAX
+
+    def c(self) -> pool2d_params_t:
+        return pool2d_params_t(self.batch, self.in_rows, self.in_cols, self.channels, self.window_rows,
+                               self.window_cols, self.stride_rows, self.stride_cols, self.padding, self.op)
+
+
+def pool2d_output_shape(p: PoolParams):
+    o = (ctypes.c_int32 * 4)()
+    pd = (ctypes.c_int32 * 4)()
+    _check(_lib.pool2d_output_shape(ctypes.byref(p.c()), o, pd), "pool2d_output_shape")
+    return tuple(o), tuple(pd)
+
+
+def pool2d_forward(p: PoolParams, x, y, stream=None) -> None:
+    """x, y: torch CUDA tensors (or raw device pointers as ints); one kernel launch."""
+    _check(_lib.pool2d_forward(ctypes.byref(p.c()), _ptr(x), _ptr(y), _stream_ptr(stream)), "pool2d_forward")
 
 
 def _check(st: int, where: str):

@@ -9,6 +9,7 @@
 // choice is cached per (params, device).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdio>
 #include <cstring>
@@ -22,6 +23,7 @@
 
 #include "internal.h"
 #include "../../include/conv2d_debug.h"
+#include "../../include/pool2d.h"
 
 using namespace conv2d;
 
@@ -638,6 +640,51 @@ const char* conv2d_algo_name(conv2d_algo_t a) {
 }
 
 const char* conv2d_last_error(void) { return g_last_error.c_str(); }
+
+// ---- pooling (include/pool2d.h): shapes via the conv algebra with F := C
+static bool pool_shape(const pool2d_params_t* p, Problem* q, std::string* why) {
+  if (!p) {
+    *why = "params is NULL";
+    return false;
+  }
+  if (p->op != POOL2D_MAX && p->op != POOL2D_AVG) {
+    *why = "bad pooling op";
+    return false;
+  }
+  conv2d_params_t c{p->batch, p->in_rows, p->in_cols, p->channels, p->channels, p->window_rows, p->window_cols,
+                    p->stride_rows, p->stride_cols, p->padding, CONV2D_MATH_FP32};
+  return shape_of(&c, q, why);
+}
+
+conv2d_status_t pool2d_output_shape(const pool2d_params_t* p, int32_t out_nhwc[4], int32_t pads_tblr[4]) {
+  Problem q;
+  std::string why;
+  if (!pool_shape(p, &q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
+  if (out_nhwc) {
+    out_nhwc[0] = q.N; out_nhwc[1] = q.HO; out_nhwc[2] = q.WO; out_nhwc[3] = q.C;
+  }
+  if (pads_tblr) {
+    pads_tblr[0] = q.pad_top;
+    pads_tblr[1] = std::max(0, (q.HO - 1) * q.SH + q.KH - q.H - q.pad_top);
+    pads_tblr[2] = q.pad_left;
+    pads_tblr[3] = std::max(0, (q.WO - 1) * q.SW + q.KW - q.W - q.pad_left);
+  }
+  return CONV2D_OK;
+}
+
+conv2d_status_t pool2d_forward(const pool2d_params_t* p, const float* in, float* out, void* stream) {
+  Problem q;
+  std::string why;
+  if (!pool_shape(p, &q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
+  if (!in || !out) return fail(CONV2D_ERR_NULL, "in/out is NULL");
+  if ((reinterpret_cast<uintptr_t>(in) & 3) || (reinterpret_cast<uintptr_t>(out) & 3))
+    return fail(CONV2D_ERR_ALIGNMENT, "pointers must be 4-byte aligned");
+  conv2d_status_t st = check_device(nullptr);
+  if (st != CONV2D_OK) return st;
+  PoolProblem pp{q.N, q.H, q.W, q.C, q.KH, q.KW, q.SH, q.SW, q.HO, q.WO, q.pad_top, q.pad_left, p->op == POOL2D_AVG};
+  cudaError_t e = launch_pool(pp, in, out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? CONV2D_OK : cuda_fail(e, "pool2d");
+}
 
 int conv2d_debug_trace(int enable, unsigned long long* host, int n) {
   return conv2d::gemm2_trace(enable, host, n);

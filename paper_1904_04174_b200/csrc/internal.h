@@ -24,6 +24,13 @@ struct Problem {
   int64_t filt_elems() const { return K() * F; }
 };
 
+// ---- pool.cu (include/pool2d.h)
+struct PoolProblem {
+  int N, H, W, C, KH, KW, SH, SW, HO, WO, PT, PL;
+  bool avg;
+};
+cudaError_t launch_pool(const PoolProblem& p, const float* x, float* y, cudaStream_t s);
+
 // ---- direct.cu
 cudaError_t launch_direct(const Problem& p, const float* in, const float* filt, float* out, cudaStream_t s);
 // ---- tiled.cu

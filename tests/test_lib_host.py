@@ -27,7 +27,7 @@ def C():
 def test_exports_every_declared_symbol(C):
     inc = os.path.join(ROOT, "include")
     hdr = "".join(open(os.path.join(inc, f)).read() for f in sorted(os.listdir(inc)) if f.endswith(".h"))
-    declared = set(re.findall(r"\b(conv2d_[a-z_]+)\s*\(", hdr))
+    declared = set(re.findall(r"\b((?:conv2d|pool2d)_[a-z_]+)\s*\(", hdr))
     declared = {d for d in declared if not d.endswith("_t")}
     assert declared == set(C.EXPORTED), declared ^ set(C.EXPORTED)
     for name in declared:
@@ -150,3 +150,29 @@ def test_selection_cache_host_side(C):
         C.conv2d_set_selected(p, C.ALGO_MATMUL_1X1)
     C.conv2d_clear_selection_cache()
     assert C.conv2d_selected(p) is None
+
+
+@pytest.mark.parametrize("case", [(2, 13, 11, 5, 3, 3, 2, 2, 0), (256, 112, 112, 64, 3, 3, 2, 2, 0),
+                                  (3, 14, 14, 4, 2, 2, 2, 2, 1), (1, 9, 10, 3, 4, 2, 3, 1, 0),
+                                  (32, 7, 7, 2048, 7, 7, 1, 1, 1)], ids=str)
+def test_pool_shapes_match_oracle(C, case):
+    n, h, w, c, kh, kw, sh, sw, pad = case
+    for op in (C.POOL_MAX, C.POOL_AVG):
+        got = C.pool2d_output_shape(C.PoolParams(n, h, w, c, kh, kw, sh, sw, pad, op))
+        assert got == O.pool_output_shape(O.PoolParams(n, h, w, c, kh, kw, sh, sw, pad, op))
+
+
+def test_pool_validation_errors_before_any_launch(C):
+    P = C.PoolParams
+    for bad, code in [(P(0, 4, 4, 1, 2, 2), "INVALID_PARAMS"), (P(1, 4, 4, 1, 5, 5, 1, 1, C.PAD_VALID), "INVALID_PARAMS"),
+                      (P(1, 4, 4, 1, 2, 2, 1, 1, C.PAD_SAME, 9), "INVALID_PARAMS"),
+                      (P(1, 4, 4, 1, 2, 2, 0, 1), "INVALID_PARAMS")]:
+        with pytest.raises(RuntimeError) as ei:
+            C.pool2d_forward(bad, 16, 16, stream=0)
+        assert code in str(ei.value)
+    with pytest.raises(RuntimeError) as ei:
+        C.pool2d_forward(P(1, 4, 4, 1, 2, 2), 0, 16, stream=0)
+    assert "NULL" in str(ei.value)
+    with pytest.raises(RuntimeError) as ei:
+        C.pool2d_forward(P(1, 4, 4, 1, 2, 2), 18, 16, stream=0)
+    assert "ALIGNMENT" in str(ei.value)
