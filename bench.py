@@ -408,7 +408,7 @@ def main():
     # dominant kernel = the tcgen05 GEMM core (gemm2sm_kernel), which runs every conv whose chosen
     # algorithm is implicit_gemm / matmul_1x1 / winograd; its per-conv time (CUDA events on the
     # launching stream, inside the timed region) includes the small filter-prep / split-reduce launches.
-    tensor_algos = (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1, C.ALGO_WINOGRAD_F2X2_3X3)
+    tensor_algos = (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1, C.ALGO_WINOGRAD_F2X2_3X3, C.ALGO_WINOGRAD_F4X4_3X3)
     grp = [(cv, ms) for cv, ms in zip(convs, per_conv_ms) if cv["algo"] in tensor_algos]
     if not grp:  # degenerate: everything picked a CUDA-core algorithm
         grp = list(zip(convs, per_conv_ms))

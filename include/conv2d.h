@@ -60,9 +60,11 @@ typedef enum {
   CONV2D_ALGO_TILED = 2,             /* CTA output tile, smem halo, register blocking */
   CONV2D_ALGO_IMPLICIT_GEMM = 3,     /* tcgen05/TMEM GEMM over the never-materialised im2col matrix */
   CONV2D_ALGO_WINOGRAD_F2X2_3X3 = 4, /* Winograd F(2x2,3x3), tensor-core batched GEMM */
-  CONV2D_ALGO_MATMUL_1X1 = 5         /* 1x1/stride-1 conv as one GEMM */
+  CONV2D_ALGO_MATMUL_1X1 = 5,        /* 1x1/stride-1 conv as one GEMM */
+  CONV2D_ALGO_WINOGRAD_F4X4_3X3 = 6  /* Winograd F(4x4,3x3) ("Winograd large"): 6x6 tiles, 36
+                                        batched tensor-core GEMMs, 4x fewer multiplies than direct */
 } conv2d_algo_t;
-#define CONV2D_NUM_ALGOS 6
+#define CONV2D_NUM_ALGOS 7
 
 typedef struct {
   int32_t batch, in_rows, in_cols, channels, features;
@@ -94,7 +96,9 @@ conv2d_status_t conv2d_flop_count(const conv2d_params_t* p, uint64_t* flops);
 /* *supported = 1 iff `algo` can run `p` (no device needed).  AUTO is always supported.
  *   DIRECT, TILED, IMPLICIT_GEMM : every valid params
  *   MATMUL_1X1                   : Kh = Kw = 1 and Sr = Sc = 1
- *   WINOGRAD_F2X2_3X3            : Kh = Kw = 3, Sr = Sc = 1, C >= 32 (reading R13/R16) */
+ *   WINOGRAD_F2X2_3X3            : Kh = Kw = 3, Sr = Sc = 1, C >= 32 (reading R13/R16)
+ *   WINOGRAD_F4X4_3X3            : as F2X2 and math = FP32 only -- in TF32 mode its larger transform
+ *                                  constants put the error at the 2e-3 bound (reading R21) */
 conv2d_status_t conv2d_supports(const conv2d_params_t* p, conv2d_algo_t algo, int* supported);
 
 /* Device workspace bytes `algo` needs for `p` (AUTO: max over supported

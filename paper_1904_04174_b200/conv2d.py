@@ -25,9 +25,10 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 PAD_SAME, PAD_VALID = 0, 1
 MATH_FP32, MATH_TF32 = 0, 1
-ALGO_AUTO, ALGO_DIRECT, ALGO_TILED, ALGO_IMPLICIT_GEMM, ALGO_WINOGRAD_F2X2_3X3, ALGO_MATMUL_1X1 = range(6)
-NUM_ALGOS = 6
-ALGO_NAMES = ["auto", "direct", "tiled", "implicit_gemm", "winograd_f2x2_3x3", "matmul_1x1"]
+(ALGO_AUTO, ALGO_DIRECT, ALGO_TILED, ALGO_IMPLICIT_GEMM, ALGO_WINOGRAD_F2X2_3X3, ALGO_MATMUL_1X1,
+ ALGO_WINOGRAD_F4X4_3X3) = range(7)
+NUM_ALGOS = 7
+ALGO_NAMES = ["auto", "direct", "tiled", "implicit_gemm", "winograd_f2x2_3x3", "matmul_1x1", "winograd_f4x4_3x3"]
 ALGO_BY_NAME = {n: i for i, n in enumerate(ALGO_NAMES)}
 
 STATUS = ["CONV2D_OK", "CONV2D_ERR_INVALID_PARAMS", "CONV2D_ERR_UNSUPPORTED", "CONV2D_ERR_WORKSPACE",

@@ -30,7 +30,7 @@ using namespace conv2d;
 namespace {
 
 thread_local std::string g_last_error;
-thread_local double g_tune_times[CONV2D_NUM_ALGOS] = {-1, -1, -1, -1, -1, -1};
+thread_local double g_tune_times[CONV2D_NUM_ALGOS] = {-1, -1, -1, -1, -1, -1, -1};
 
 conv2d_status_t fail(conv2d_status_t s, const std::string& msg) {
   g_last_error = msg;
@@ -107,6 +107,8 @@ bool algo_supports(const Problem& q, conv2d_algo_t a) {
       return q.KH == 1 && q.KW == 1 && q.SH == 1 && q.SW == 1;
     case CONV2D_ALGO_WINOGRAD_F2X2_3X3:
       return q.KH == 3 && q.KW == 3 && q.SH == 1 && q.SW == 1 && q.C >= 32;
+    case CONV2D_ALGO_WINOGRAD_F4X4_3X3:  // FP32 math only (reading R21)
+      return q.KH == 3 && q.KW == 3 && q.SH == 1 && q.SW == 1 && q.C >= 32 && q.math == CONV2D_MATH_FP32;
   }
   return false;
 }
@@ -115,7 +117,8 @@ size_t algo_workspace(const Problem& q, conv2d_algo_t a) {
   switch (a) {
     case CONV2D_ALGO_IMPLICIT_GEMM: return igemm_workspace(q, false);
     case CONV2D_ALGO_MATMUL_1X1: return igemm_workspace(q, true);
-    case CONV2D_ALGO_WINOGRAD_F2X2_3X3: return winograd_workspace(q);
+    case CONV2D_ALGO_WINOGRAD_F2X2_3X3: return winograd_workspace(q, 2);
+    case CONV2D_ALGO_WINOGRAD_F4X4_3X3: return winograd_workspace(q, 4);
     default: return 0;
   }
 }
@@ -126,7 +129,8 @@ int algo_launches(const Problem& q, conv2d_algo_t a) {
     case CONV2D_ALGO_TILED: return 1;
     case CONV2D_ALGO_IMPLICIT_GEMM: return igemm_launches(q, false);
     case CONV2D_ALGO_MATMUL_1X1: return igemm_launches(q, true);
-    case CONV2D_ALGO_WINOGRAD_F2X2_3X3: return winograd_launches(q);
+    case CONV2D_ALGO_WINOGRAD_F2X2_3X3: return winograd_launches(q, 2);
+    case CONV2D_ALGO_WINOGRAD_F4X4_3X3: return winograd_launches(q, 4);
     default: return -1;
   }
 }
@@ -171,7 +175,8 @@ conv2d_status_t run_algo(const Problem& q, conv2d_algo_t a, const float* in, con
     case CONV2D_ALGO_TILED: e = launch_tiled(q, in, filt, out, s); break;
     case CONV2D_ALGO_IMPLICIT_GEMM: e = launch_igemm(q, false, in, filt, out, ws, s); break;
     case CONV2D_ALGO_MATMUL_1X1: e = launch_igemm(q, true, in, filt, out, ws, s); break;
-    case CONV2D_ALGO_WINOGRAD_F2X2_3X3: e = launch_winograd(q, in, filt, out, ws, s); break;
+    case CONV2D_ALGO_WINOGRAD_F2X2_3X3: e = launch_winograd(q, 2, in, filt, out, ws, s); break;
+    case CONV2D_ALGO_WINOGRAD_F4X4_3X3: e = launch_winograd(q, 4, in, filt, out, ws, s); break;
     default: return fail(CONV2D_ERR_UNSUPPORTED, "no algorithm to run");
   }
   if (e != cudaSuccess) return cuda_fail(e, conv2d_algo_name(a));
@@ -634,6 +639,7 @@ const char* conv2d_algo_name(conv2d_algo_t a) {
     case CONV2D_ALGO_TILED: return "tiled";
     case CONV2D_ALGO_IMPLICIT_GEMM: return "implicit_gemm";
     case CONV2D_ALGO_WINOGRAD_F2X2_3X3: return "winograd_f2x2_3x3";
+    case CONV2D_ALGO_WINOGRAD_F4X4_3X3: return "winograd_f4x4_3x3";
     case CONV2D_ALGO_MATMUL_1X1: return "matmul_1x1";
   }
   return "unknown";

@@ -44,9 +44,9 @@ int igemm_launches(const Problem& p, bool is_1x1);
 cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const float* filt, float* out, void* ws,
                          cudaStream_t s);
 // ---- winograd.cu
-size_t winograd_workspace(const Problem& p);
-int winograd_launches(const Problem& p);
-cudaError_t launch_winograd(const Problem& p, const float* in, const float* filt, float* out, void* ws,
+size_t winograd_workspace(const Problem& p, int mt);  // mt = output tile: 2 (F2x2) or 4 (F4x4)
+int winograd_launches(const Problem& p, int mt);
+cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const float* filt, float* out, void* ws,
                             cudaStream_t s);
 // ---- synth.cu
 cudaError_t launch_synth_fill(float* dst, uint64_t count, uint64_t key, uint64_t offset, int dist, cudaStream_t s);

@@ -1,4 +1,6 @@
-// winograd.cu -- CONV2D_ALGO_WINOGRAD_F2X2_3X3: "a tiled Winograd operation which uses
+// winograd.cu -- CONV2D_ALGO_WINOGRAD_F2X2_3X3 and CONV2D_ALGO_WINOGRAD_F4X4_3X3 (the
+// "Winograd large" variant; same pipeline with 6x6 tiles, 36 batched GEMMs, 4x fewer multiplies than
+// direct; FP32 math only -- DESIGN.md reading R21): "a tiled Winograd operation which uses
 // data transforms to convert the convolution into a number of small matrix multiplies,
 // reducing the total number of floating point operations" (
 // SPEC.md:258-266; Lavin & Gray F(2x2,3x3), correlation form, reading R12):
@@ -33,46 +35,88 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
-// U_xi stored K-major per xi: Ut[xi][f][c], Fpad rows x Cpad cols.
+// 1-D transforms of one column (applied along both axes).
+// F(2x2,3x3) (Lavin-Gray): G g, B^T d, A^T m
+__device__ __forceinline__ void g2(const float* g, float* u) {
+  u[0] = g[0];
+  u[1] = 0.5f * (g[0] + g[1] + g[2]);
+  u[2] = 0.5f * (g[0] - g[1] + g[2]);
+  u[3] = g[2];
+}
+__device__ __forceinline__ void bt2(const float* d, float* v) {
+  v[0] = d[0] - d[2];
+  v[1] = d[1] + d[2];
+  v[2] = d[2] - d[1];
+  v[3] = d[1] - d[3];
+}
+__device__ __forceinline__ void at2(const float* m, float* y) {
+  y[0] = m[0] + m[1] + m[2];
+  y[1] = m[1] - m[2] - m[3];
+}
+// F(4x4,3x3) (Lavin-Gray, points 0, +-1, +-2, inf):
+//   G   = [[1/4,0,0],[-1/6,-1/6,-1/6],[-1/6,1/6,-1/6],[1/24,1/12,1/6],[1/24,-1/12,1/6],[0,0,1]]
+//   B^T = [[4,0,-5,0,1,0],[0,-4,-4,1,1,0],[0,4,-4,-1,1,0],[0,-2,-1,2,1,0],[0,2,-1,-2,1,0],[0,4,0,-5,0,1]]
+//   A^T = [[1,1,1,1,1,0],[0,1,-1,2,-2,0],[0,1,1,4,4,0],[0,1,-1,8,-8,1]]
+__device__ __forceinline__ void g4(const float* g, float* u) {
+  u[0] = 0.25f * g[0];
+  u[1] = -(g[0] + g[1] + g[2]) * (1.f / 6.f);
+  u[2] = -(g[0] - g[1] + g[2]) * (1.f / 6.f);
+  u[3] = g[0] * (1.f / 24.f) + g[1] * (1.f / 12.f) + g[2] * (1.f / 6.f);
+  u[4] = g[0] * (1.f / 24.f) - g[1] * (1.f / 12.f) + g[2] * (1.f / 6.f);
+  u[5] = g[2];
+}
+__device__ __forceinline__ void bt4(const float* d, float* v) {
+  v[0] = 4.f * d[0] - 5.f * d[2] + d[4];
+  v[1] = -4.f * d[1] - 4.f * d[2] + d[3] + d[4];
+  v[2] = 4.f * d[1] - 4.f * d[2] - d[3] + d[4];
+  v[3] = -2.f * d[1] - d[2] + 2.f * d[3] + d[4];
+  v[4] = 2.f * d[1] - d[2] - 2.f * d[3] + d[4];
+  v[5] = 4.f * d[1] - 5.f * d[3] + d[5];
+}
+__device__ __forceinline__ void at4(const float* m, float* y) {
+  y[0] = m[0] + m[1] + m[2] + m[3] + m[4];
+  y[1] = m[1] - m[2] + 2.f * m[3] - 2.f * m[4];
+  y[2] = m[1] + m[2] + 4.f * m[3] + 4.f * m[4];
+  y[3] = m[1] - m[2] + 8.f * m[3] - 8.f * m[4] + m[5];
+}
+template <int MT> __device__ __forceinline__ void gT(const float* g, float* u) { if (MT == 2) g2(g, u); else g4(g, u); }
+template <int MT> __device__ __forceinline__ void bT(const float* d, float* v) { if (MT == 2) bt2(d, v); else bt4(d, v); }
+template <int MT> __device__ __forceinline__ void aT(const float* m, float* y) { if (MT == 2) at2(m, y); else at4(m, y); }
+
+// U_xi stored K-major per xi: Ut[xi][f][c], Fpad rows x Cpad cols; U = G g G^T (ALPHA x ALPHA)
+template <int MT>
 __global__ void wino_filter_kernel(const float* __restrict__ w, int C, int F, int64_t cpad, int64_t fpad,
                                    float* __restrict__ ut_hi, float* __restrict__ ut_lo, int mode /*0 3x,1 tf32*/) {
   pdl_trigger();
   pdl_wait();
+  constexpr int AL = MT + 2;
   const int64_t total = cpad * fpad;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int f = (int)(i % fpad);
     const int c = (int)(i / fpad);
-    float u[4][4];
+    float u[AL][AL];
     if (c < C && f < F) {
-      float g[3][3];
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int s = 0; s < 3; ++s) g[r][s] = w[((int64_t)(r * 3 + s) * C + c) * F + f];
-      float t[4][3];  // G g
+      float t[AL][3];  // G g, column by column
 #pragma unroll
       for (int s = 0; s < 3; ++s) {
-        t[0][s] = g[0][s];
-        t[1][s] = 0.5f * (g[0][s] + g[1][s] + g[2][s]);
-        t[2][s] = 0.5f * (g[0][s] - g[1][s] + g[2][s]);
-        t[3][s] = g[2][s];
+        float col[3], out[AL];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) col[r] = w[((int64_t)(r * 3 + s) * C + c) * F + f];
+        gT<MT>(col, out);
+#pragma unroll
+        for (int r = 0; r < AL; ++r) t[r][s] = out[r];
       }
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {  // (G g) G^T
-        u[r][0] = t[r][0];
-        u[r][1] = 0.5f * (t[r][0] + t[r][1] + t[r][2]);
-        u[r][2] = 0.5f * (t[r][0] - t[r][1] + t[r][2]);
-        u[r][3] = t[r][2];
-      }
+      for (int r = 0; r < AL; ++r) gT<MT>(t[r], u[r]);  // (G g) G^T
     } else {
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+      for (int r = 0; r < AL; ++r)
 #pragma unroll
-        for (int s = 0; s < 4; ++s) u[r][s] = 0.f;
+        for (int s = 0; s < AL; ++s) u[r][s] = 0.f;
     }
 #pragma unroll
-    for (int xi = 0; xi < 16; ++xi) {
-      const float v = u[xi / 4][xi % 4];
+    for (int xi = 0; xi < AL * AL; ++xi) {
+      const float v = u[xi / AL][xi % AL];
       const int64_t o = ((int64_t)xi * fpad + f) * cpad + c;
       if (mode == 0) {
         const float h = sm100::tf32_hi(v);
@@ -85,11 +129,14 @@ __global__ void wino_filter_kernel(const float* __restrict__ w, int C, int F, in
   }
 }
 
-// V[xi][t][c] (row stride cpad), t = (n, th, tw)
+// V[xi][t][c] (row stride cpad), t = (n, th, tw); V = B^T d B over the ALPHA x ALPHA input tile at
+// (MT*th - PT, MT*tw - PL) (tiles overlap by 2)
+template <int MT>
 __global__ void wino_input_kernel(const float* __restrict__ x, int H, int W, int C, int TH, int TW, int PT, int PL,
                                   int64_t T, int64_t cpad, float* __restrict__ V, int round_rna) {
   pdl_trigger();
   pdl_wait();
+  constexpr int AL = MT + 2;
   const int64_t total = T * cpad;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % cpad);
@@ -97,74 +144,82 @@ __global__ void wino_input_kernel(const float* __restrict__ x, int H, int W, int
     const int tw = (int)(t % TW);
     const int th = (int)((t / TW) % TH);
     const int64_t n = t / ((int64_t)TW * TH);
-    float d[4][4];
-    const int h0 = 2 * th - PT, w0 = 2 * tw - PL;
+    float d[AL][AL];
+    const int h0 = MT * th - PT, w0 = MT * tw - PL;
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < AL; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
+      for (int b = 0; b < AL; ++b) {
         const int ih = h0 + a, iw = w0 + b;
         d[a][b] = (c < C && ih >= 0 && ih < H && iw >= 0 && iw < W) ? x[((n * H + ih) * W + iw) * C + c] : 0.f;
       }
-    float q[4][4];  // B^T d
+    float q[AL][AL];  // B^T d, column by column
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      q[0][b] = d[0][b] - d[2][b];
-      q[1][b] = d[1][b] + d[2][b];
-      q[2][b] = d[2][b] - d[1][b];
-      q[3][b] = d[1][b] - d[3][b];
+    for (int b = 0; b < AL; ++b) {
+      float col[AL], out[AL];
+#pragma unroll
+      for (int a = 0; a < AL; ++a) col[a] = d[a][b];
+      bT<MT>(col, out);
+#pragma unroll
+      for (int a = 0; a < AL; ++a) q[a][b] = out[a];
     }
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {  // (B^T d) B
-      const float v0 = q[a][0] - q[a][2];
-      const float v1 = q[a][1] + q[a][2];
-      const float v2 = q[a][2] - q[a][1];
-      const float v3 = q[a][1] - q[a][3];
-      const float vv[4] = {v0, v1, v2, v3};
+    for (int a = 0; a < AL; ++a) {  // (B^T d) B
+      float vv[AL];
+      bT<MT>(q[a], vv);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
+      for (int b = 0; b < AL; ++b) {
         const float v = round_rna ? tf32_rna(vv[b]) : vv[b];
-        V[((int64_t)(a * 4 + b) * T + t) * cpad + c] = v;
+        V[((int64_t)(a * AL + b) * T + t) * cpad + c] = v;
       }
     }
   }
 }
 
-// Y tile = A^T M A, M[xi][t][f] (row stride ldm)
+// Y tile (MT x MT) = A^T M A, M[xi][t][f] (row stride ldm)
+template <int MT>
 __global__ void wino_output_kernel(const float* __restrict__ Mw, int64_t T, int64_t ldm, int F, int HO, int WO,
                                    int TH, int TW, float* __restrict__ y) {
   pdl_trigger();
   pdl_wait();
+  constexpr int AL = MT + 2;
   const int64_t total = T * F;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int f = (int)(i % F);
     const int64_t t = i / F;
-    float m[4][4];
+    float m[AL][AL];
 #pragma unroll
-    for (int xi = 0; xi < 16; ++xi) m[xi / 4][xi % 4] = Mw[((int64_t)xi * T + t) * ldm + f];
-    float r[2][4];  // A^T M
+    for (int xi = 0; xi < AL * AL; ++xi) m[xi / AL][xi % AL] = Mw[((int64_t)xi * T + t) * ldm + f];
+    float r[MT][AL];  // A^T M, column by column
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      r[0][b] = m[0][b] + m[1][b] + m[2][b];
-      r[1][b] = m[1][b] - m[2][b] - m[3][b];
+    for (int b = 0; b < AL; ++b) {
+      float col[AL], out[MT];
+#pragma unroll
+      for (int a = 0; a < AL; ++a) col[a] = m[a][b];
+      aT<MT>(col, out);
+#pragma unroll
+      for (int a = 0; a < MT; ++a) r[a][b] = out[a];
     }
     const int tw = (int)(t % TW);
     const int th = (int)((t / TW) % TH);
     const int64_t n = t / ((int64_t)TW * TH);
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      const float y0 = r[a][0] + r[a][1] + r[a][2];
-      const float y1 = r[a][1] - r[a][2] - r[a][3];
-      const int ho = 2 * th + a;
+    for (int a = 0; a < MT; ++a) {
+      float yy[MT];
+      aT<MT>(r[a], yy);  // (A^T M) A
+      const int ho = MT * th + a;
       if (ho >= HO) continue;
-      const int wo = 2 * tw;
-      y[((n * HO + ho) * WO + wo) * F + f] = y0;
-      if (wo + 1 < WO) y[((n * HO + ho) * WO + wo + 1) * F + f] = y1;
+#pragma unroll
+      for (int b = 0; b < MT; ++b) {
+        const int wo = MT * tw + b;
+        if (wo < WO) y[((n * HO + ho) * WO + wo) * F + f] = yy[b];
+      }
     }
   }
 }
 
 struct WPlan {
+  int mt, xi;  // output tile MT x MT, XI = (MT + 2)^2 transformed points = batched GEMMs
   bool three_x;
   int block_n, splits;
   int TH, TW;
@@ -172,21 +227,23 @@ struct WPlan {
   size_t ut_bytes, v_bytes, m_bytes, partial_bytes, total;
 };
 
-WPlan make_wplan(const Problem& p) {
+WPlan make_wplan(const Problem& p, int mt) {
   WPlan w{};
+  w.mt = mt;
+  w.xi = (mt + 2) * (mt + 2);
   w.three_x = p.math == CONV2D_MATH_FP32;
-  w.TH = (p.HO + 1) / 2;
-  w.TW = (p.WO + 1) / 2;
+  w.TH = (p.HO + mt - 1) / mt;
+  w.TW = (p.WO + mt - 1) / mt;
   w.T = (int64_t)p.N * w.TH * w.TW;
   w.cpad = round_up(p.C, 32);
   w.block_n = gemm2_choose_block_n(p.F);
   w.fpad = round_up(p.F, w.block_n);
   w.ldm = round_up(p.F, 4);
-  w.splits = gemm2_choose_splits(w.T, p.F, (int)(w.cpad / 32), 16, w.block_n);
+  w.splits = gemm2_choose_splits(w.T, p.F, (int)(w.cpad / 32), w.xi, w.block_n);
   if (w.ldm != p.F) w.splits = 1;
-  w.ut_bytes = round_up(16 * w.fpad * w.cpad * 4, 256);
-  w.v_bytes = round_up(16 * w.T * w.cpad * 4, 256);
-  w.m_bytes = round_up(16 * w.T * w.ldm * 4, 256);
+  w.ut_bytes = round_up(w.xi * w.fpad * w.cpad * 4, 256);
+  w.v_bytes = round_up(w.xi * w.T * w.cpad * 4, 256);
+  w.m_bytes = round_up(w.xi * w.T * w.ldm * 4, 256);
   w.partial_bytes = w.splits > 1 ? (size_t)w.splits * w.m_bytes : 0;
   w.total = w.ut_bytes * (w.three_x ? 2 : 1) + w.v_bytes + w.m_bytes + w.partial_bytes;
   return w;
@@ -200,12 +257,12 @@ unsigned grid_for(int64_t total) {
 
 }  // namespace
 
-size_t winograd_workspace(const Problem& p) { return make_wplan(p).total; }
-int winograd_launches(const Problem& p) { return 4 + (make_wplan(p).splits > 1 ? 1 : 0); }
+size_t winograd_workspace(const Problem& p, int mt) { return make_wplan(p, mt).total; }
+int winograd_launches(const Problem& p, int mt) { return 4 + (make_wplan(p, mt).splits > 1 ? 1 : 0); }
 
-cudaError_t launch_winograd(const Problem& p, const float* in, const float* filt, float* out, void* ws,
+cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const float* filt, float* out, void* ws,
                             cudaStream_t s) {
-  const WPlan w = make_wplan(p);
+  const WPlan w = make_wplan(p, mt);
   uint8_t* b = static_cast<uint8_t*>(ws);
   float* ut_hi = reinterpret_cast<float*>(b);
   b += w.ut_bytes;
@@ -220,11 +277,14 @@ cudaError_t launch_winograd(const Problem& p, const float* in, const float* filt
   b += w.m_bytes;
   float* partial = w.splits > 1 ? reinterpret_cast<float*>(b) : nullptr;
 
-  cudaError_t e = launch_k(wino_filter_kernel, dim3(grid_for(w.cpad * w.fpad)), dim3(256), 0, s, filt, p.C, p.F,
-                           w.cpad, w.fpad, ut_hi, ut_lo, w.three_x ? 0 : 1);
+  auto kf = mt == 2 ? wino_filter_kernel<2> : wino_filter_kernel<4>;
+  auto ki = mt == 2 ? wino_input_kernel<2> : wino_input_kernel<4>;
+  auto ko = mt == 2 ? wino_output_kernel<2> : wino_output_kernel<4>;
+  cudaError_t e = launch_k(kf, dim3(grid_for(w.cpad * w.fpad)), dim3(256), 0, s, filt, p.C, p.F, w.cpad, w.fpad,
+                           ut_hi, ut_lo, w.three_x ? 0 : 1);
   if (e != cudaSuccess) return e;
-  e = launch_k(wino_input_kernel, dim3(grid_for(w.T * w.cpad)), dim3(256), 0, s, in, p.H, p.W, p.C, w.TH, w.TW,
-               p.pad_top, p.pad_left, w.T, w.cpad, V, w.three_x ? 0 : 1);
+  e = launch_k(ki, dim3(grid_for(w.T * w.cpad)), dim3(256), 0, s, in, p.H, p.W, p.C, w.TH, w.TW, p.pad_top,
+               p.pad_left, w.T, w.cpad, V, w.three_x ? 0 : 1);
   if (e != cudaSuccess) return e;
   Gemm2Args g{};
   g.a_mode = A_DENSE;
@@ -241,14 +301,13 @@ cudaError_t launch_winograd(const Problem& p, const float* in, const float* filt
   g.partial = partial;
   g.M = w.T;
   g.N = p.F;
-  g.batch = 16;
+  g.batch = w.xi;
   g.splits = w.splits;
   g.three_x = w.three_x;
   g.block_n = w.block_n;
   e = launch_gemm2(p, g, s);
   if (e != cudaSuccess) return e;
-  return launch_k(wino_output_kernel, dim3(grid_for(w.T * p.F)), dim3(256), 0, s, Mw, w.T, w.ldm, p.F, p.HO, p.WO,
-                  w.TH, w.TW, out);
+  return launch_k(ko, dim3(grid_for(w.T * p.F)), dim3(256), 0, s, Mw, w.T, w.ldm, p.F, p.HO, p.WO, w.TH, w.TW, out);
 }
 
 }  // namespace conv2d

@@ -71,3 +71,13 @@ def check_close(p, y: np.ndarray, y_ref: np.ndarray, denom: np.ndarray, algo: in
     tol = tol_for(algo, p.math)
     assert e <= tol, f"{what}: normalized error {e:.3e} > {tol:.0e}"
     return e
+
+
+def assert_int_exact(p, y: np.ndarray, y_ref: np.ndarray, denom: np.ndarray, algo: int, what: str = ""):
+    """Integer regime (inputs in {-2..2}): every partial sum is exact, so every algorithm is bit-exact --
+    except Winograd F(4x4,3x3), whose filter transform has non-dyadic constants (1/6, 1/12, 1/24) and is
+    held to the fp32 tolerance instead (reading R21)."""
+    if algo == C().ALGO_WINOGRAD_F4X4_3X3:
+        check_close(p, y, y_ref, denom, algo, what)
+    else:
+        assert np.array_equal(y, y_ref), (what, int(np.sum(y != y_ref)))

@@ -12,7 +12,7 @@ import oracle as O
 from paper_1904_04174_b200 import layers as L
 from paper_1904_04174_b200 import synth
 
-from .parity import C, check_close, gpu_conv, make_inputs, oparams, supported_algos
+from .parity import C, assert_int_exact, check_close, gpu_conv, make_inputs, oparams, supported_algos
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -48,16 +48,16 @@ ALL_SHAPES = [l for l in L.RESNET50_SETS] + [l for l, _ in L.VGG16_LAYERS]
 
 @pytest.mark.parametrize("layer", ALL_SHAPES, ids=lambda l: l.name)
 def test_exact_integer_regime_b1(cuda_ok, layer):
-    """P7: integer data in [-2,2] makes every partial sum exact -> every algorithm bit-exact."""
+    """P7: integer data in [-2,2] makes every partial sum exact -> every algorithm bit-exact (F(4x4):
+    tolerance, reading R21)."""
     p0 = C().Params(**layer.params(1))
     x, w = make_inputs(p0, layer_id=100, dist=synth.DIST_INT5)
-    ref = O.conv2d(oparams(p0), x, w)
+    ref, den = O.conv2d(oparams(p0), x, w, with_denom=True)
     for math in MATHS:
         p = p0.replace(math=math)
         for a in supported_algos(p):
             y = gpu_conv(p, x, w, a)
-            assert np.array_equal(y, ref), (layer.name, math, C().conv2d_algo_name(a),
-                                            int(np.sum(y != ref)))
+            assert_int_exact(p, y, ref, den, a, f"{layer.name} math={math} {C().conv2d_algo_name(a)}")
 
 
 @pytest.mark.parametrize("layer", ALL_SHAPES, ids=lambda l: l.name)
@@ -144,12 +144,12 @@ def test_edge_cases(cuda_ok, case):
     x, w = make_inputs(p0, layer_id=400)
     ref, den = O.conv2d(oparams(p0), x, w, with_denom=True)
     xi, wi = make_inputs(p0, layer_id=401, dist=synth.DIST_INT5)
-    refi = O.conv2d(oparams(p0), xi, wi)
+    refi, deni = O.conv2d(oparams(p0), xi, wi, with_denom=True)
     for math in MATHS:
         p = p0.replace(math=math)
         for a in supported_algos(p):
             check_close(p, gpu_conv(p, x, w, a), ref, den, a, f"edge {case} math={math} {C().conv2d_algo_name(a)}")
-            assert np.array_equal(gpu_conv(p, xi, wi, a), refi), (case, math, a)
+            assert_int_exact(p, gpu_conv(p, xi, wi, a), refi, deni, a, f"edge int {case} {math} {a}")
 
 
 def test_determinism_and_shard_bitwise(cuda_ok):
@@ -243,14 +243,14 @@ def test_algorithm_parameter_variants(cuda_ok, monkeypatch, variant, case):
     x, w = make_inputs(p0, layer_id=900)
     ref, den = O.conv2d(oparams(p0), x, w, with_denom=True)
     xi, wi = make_inputs(p0, layer_id=901, dist=synth.DIST_INT5)
-    refi = O.conv2d(oparams(p0), xi, wi)
+    refi, deni = O.conv2d(oparams(p0), xi, wi, with_denom=True)
     for math in MATHS:
         p = p0.replace(math=math)
         for a in (C().ALGO_IMPLICIT_GEMM, C().ALGO_MATMUL_1X1):
             if not C().conv2d_supports(p, a):
                 continue
             check_close(p, gpu_conv(p, x, w, a), ref, den, a, f"variant {variant} {case} {math} {a}")
-            assert np.array_equal(gpu_conv(p, xi, wi, a), refi)
+            assert_int_exact(p, gpu_conv(p, xi, wi, a), refi, deni, a, f"variant int {case} {a}")
 
 
 def test_selection_table_gpu_round_trip(cuda_ok, tmp_path):

@@ -37,10 +37,13 @@ def test_exports_every_declared_symbol(C):
 def test_enum_values_match_header(C):
     hdr = open(os.path.join(ROOT, "include", "conv2d.h")).read()
     for name, val in [("CONV2D_ALGO_DIRECT", 1), ("CONV2D_ALGO_TILED", 2), ("CONV2D_ALGO_IMPLICIT_GEMM", 3),
-                      ("CONV2D_ALGO_WINOGRAD_F2X2_3X3", 4), ("CONV2D_ALGO_MATMUL_1X1", 5)]:
+                      ("CONV2D_ALGO_WINOGRAD_F2X2_3X3", 4), ("CONV2D_ALGO_MATMUL_1X1", 5),
+                      ("CONV2D_ALGO_WINOGRAD_F4X4_3X3", 6)]:
         assert re.search(rf"{name}\s*=\s*{val}\b", hdr)
         assert getattr(C, name.replace("CONV2D_", "")) == val
     assert C.conv2d_algo_name(C.ALGO_WINOGRAD_F2X2_3X3) == "winograd_f2x2_3x3"
+    assert C.conv2d_algo_name(C.ALGO_WINOGRAD_F4X4_3X3) == "winograd_f4x4_3x3"
+    assert re.search(r"#define CONV2D_NUM_ALGOS 7\b", hdr) and C.NUM_ALGOS == 7
     assert C.conv2d_status_string(C.ERR_WORKSPACE) == "CONV2D_ERR_WORKSPACE"
 
 
@@ -79,6 +82,10 @@ def test_supports_table(C):
     assert not C.conv2d_supports(p3, C.ALGO_MATMUL_1X1)  # SPEC.md:257 K=3 -> incompatible
     assert not C.conv2d_supports(p3.replace(channels=3), C.ALGO_WINOGRAD_F2X2_3X3)  # reading R16: C >= 32
     assert not C.conv2d_supports(p3.replace(stride_rows=2, stride_cols=2), C.ALGO_WINOGRAD_F2X2_3X3)
+    assert C.conv2d_supports(p3, C.ALGO_WINOGRAD_F4X4_3X3)                       # FP32 math
+    assert not C.conv2d_supports(p3.replace(math=C.MATH_TF32), C.ALGO_WINOGRAD_F4X4_3X3)  # reading R21
+    assert not C.conv2d_supports(p3.replace(channels=16), C.ALGO_WINOGRAD_F4X4_3X3)
+    assert not C.conv2d_supports(p3.replace(window_rows=5, window_cols=5), C.ALGO_WINOGRAD_F4X4_3X3)
     p1 = P(1, 56, 56, 64, 256, 1, 1, 1, 1)
     assert C.conv2d_supports(p1, C.ALGO_MATMUL_1X1)
     assert not C.conv2d_supports(p1.replace(stride_rows=2, stride_cols=2), C.ALGO_MATMUL_1X1)
