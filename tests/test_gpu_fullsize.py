@@ -93,3 +93,39 @@ def test_synth_input_equals_host_generator_at_size(cuda_ok):
     xh = x.cpu().numpy()
     assert np.array_equal(xh[:100000], synth.draw(100000, key, 0))
     assert np.array_equal(xh[-100000:], synth.draw(100000, key, count - 100000))
+
+
+@pytest.mark.parametrize("k,f", [(1, 32), (3, 32)], ids=["1x1", "3x3"])
+def test_input_beyond_2e31_elements(cuda_ok, k, f):
+    """Maximum sizes (reading R20): an input of 65 x 512 x 512 x 128 = 2.18e9 elements (8.7 GB, > 2^31)
+    through every supported algorithm (FP32 math), sampled against the oracle's point evaluation.
+    Exercises the 64-bit offsets of every kernel and the TMA maps' 32-bit per-dimension coordinates."""
+    import torch
+    c = C()
+    n, h, wd, ch = 65, 512, 512, 128
+    p = c.Params(n, h, wd, ch, f, k, k, 1, 1, c.PAD_SAME)
+    assert n * h * wd * ch > 2 ** 31
+    (_, ho, wo, _), _ = c.conv2d_output_shape(p)
+    x = torch.empty(n * h * wd * ch, device="cuda")
+    c.conv2d_synth_fill(x, x.numel(), synth.stream_key(synth.SEED, 1300 + k, synth.ROLE_INPUT), 0, 0)
+    w = torch.empty(k * k * ch * f, device="cuda")
+    c.conv2d_synth_fill(w, w.numel(), synth.stream_key(synth.SEED, 1300 + k, synth.ROLE_FILTER), 0, 0)
+    y = torch.empty(n * ho * wo * f, device="cuda")
+    xh = x.view(n, h, wd, ch).cpu().numpy()
+    wh = w.view(k, k, ch, f).cpu().numpy()
+    rng = np.random.default_rng(k)
+    idx = _sample_idx(rng, n, ho, wo, f, 400)
+    ref, den = O.conv2d_points(O.Params(n, h, wd, ch, f, k, k, 1, 1, O.SAME), xh, wh, idx)
+    for a in range(1, c.NUM_ALGOS):
+        if not c.conv2d_supports(p, a):
+            continue
+        need = c.conv2d_query_workspace(p, a)
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device="cuda")
+        y.fill_(float("nan"))
+        c.conv2d_forward(p, a, x, w, y, ws, ws.numel())
+        torch.cuda.synchronize()
+        del ws
+        got = y.view(n, ho, wo, f)[idx[:, 0], idx[:, 1], idx[:, 2], idx[:, 3]].cpu().numpy().astype(np.float64)
+        e = float(np.max(np.abs(got - ref) / den))
+        assert e <= TOL_FP32, f"{c.ALGO_NAMES[a]} {k}x{k}: err {e:.3e}"
+        torch.cuda.empty_cache()
