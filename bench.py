@@ -298,6 +298,7 @@ def main():
     # ---- auto-selection (measured, once per distinct layer); rank 0's choices broadcast so every
     #      rank runs the same kernels (off the timed path)
     chosen = {}
+    C.conv2d_set_autotune_flush(flush)  # cache-cold candidate timings, as in the timed step
     if args.load_selection:
         C.conv2d_load_selection(args.load_selection)
     for cv in convs:
@@ -308,6 +309,7 @@ def main():
                                                                         ws.numel())
     if args.save_selection and rank == 0:
         C.conv2d_save_selection(args.save_selection)
+    C.conv2d_set_autotune_flush(None)
     chosen = broadcast_choices(chosen, dist if world > 1 else None, dev)
     for cv in convs:
         C.conv2d_set_selected(cv["p"], chosen[cv["layer"].name])

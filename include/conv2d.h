@@ -131,6 +131,14 @@ conv2d_status_t conv2d_set_selected(const conv2d_params_t* p, conv2d_algo_t algo
 /* Drop every cached choice. */
 void conv2d_clear_selection_cache(void);
 
+/* Cache-cold auto-selection: register a caller-owned DEVICE scratch buffer (e.g. 256 MiB, larger than the
+ * 126 MB L2) that conv2d_autotune / conv2d_forward(AUTO) overwrite with cudaMemsetAsync before every timed
+ * repetition, outside the timed events -- so candidates are compared with the cold caches a layer sees
+ * inside a network rather than with their own inputs still in L2.  buf = NULL disables it (default).
+ * The library keeps the pointer (the caller keeps the buffer alive while tuning may run) but never
+ * allocates it.  CONV2D_ERR_INVALID_PARAMS if buf != NULL and bytes == 0. */
+conv2d_status_t conv2d_set_autotune_flush(void* buf, size_t bytes);
+
 /* Persisted selector table ("table serialization round-trips", SPEC.md:354's line format with
  * this library's full cache key).  One line per cached choice of the current device:
  *     N H W C F KH KW SH SW same|valid fp32|tf32 : algorithm[/variant]

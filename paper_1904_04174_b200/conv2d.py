@@ -41,7 +41,7 @@ EXPORTED = ["conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv
             "conv2d_clear_selection_cache", "conv2d_last_tune_times", "conv2d_launch_count",
             "conv2d_synth_fill", "conv2d_status_string", "conv2d_algo_name", "conv2d_last_error",
             "conv2d_debug_trace", "conv2d_save_selection", "conv2d_load_selection",
-            "pool2d_output_shape", "pool2d_forward"]
+            "pool2d_output_shape", "pool2d_forward", "conv2d_set_autotune_flush"]
 
 
 class conv2d_params_t(ctypes.Structure):
@@ -80,6 +80,7 @@ _lib.conv2d_algo_name.restype = ctypes.c_char_p
 _lib.conv2d_last_error.argtypes = []
 _lib.conv2d_debug_trace.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 _lib.conv2d_save_selection.argtypes = [ctypes.c_char_p]
+_lib.conv2d_set_autotune_flush.argtypes = [_vp, ctypes.c_size_t]
 _lib.conv2d_load_selection.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int)]
 _lib.conv2d_debug_trace.restype = ctypes.c_int
 _lib.conv2d_last_error.restype = ctypes.c_char_p
@@ -256,6 +257,17 @@ def conv2d_status_string(s: int) -> str:
 
 def conv2d_last_error() -> str:
     return _lib.conv2d_last_error().decode()
+
+
+def conv2d_set_autotune_flush(buf, nbytes: int | None = None) -> None:
+    """Register (or with buf=None clear) a device scratch buffer the auto-selector overwrites before every
+    timed repetition (cache-cold tuning).  buf: torch CUDA tensor or raw pointer."""
+    if buf is None:
+        _check(_lib.conv2d_set_autotune_flush(None, 0), "conv2d_set_autotune_flush")
+        return
+    if nbytes is None:
+        nbytes = buf.numel() * buf.element_size()
+    _check(_lib.conv2d_set_autotune_flush(_ptr(buf), int(nbytes)), "conv2d_set_autotune_flush")
 
 
 def conv2d_save_selection(path: str) -> None:

@@ -22,8 +22,10 @@
 //     each A stage (hi = the raw fp32 stage itself: the tensor core reads only its top 19
 //     bits); B's split comes from filter_prep; the MMA warp issues lo*hi + hi*lo + hi*hi
 //     per K=8 step.
-// Warp roles (320 threads): 0-3 transform/gather, 4 TMA producer, 5 MMA issuer + TMEM
-// allocator, 6-9 epilogue (TMEM -> registers -> global, 32 columns per tcgen05.ld).
+// Warp roles (448 threads): 0-3 transform/gather, 4 TMA producer, 5 MMA issuer + TMEM
+// allocator, 6-9 epilogue (TMEM -> registers -> global, 32 columns per tcgen05.ld), 10-13 B-lo split
+// (3xTF32 with B streamed straight from the filter: lo = b - trunc(b) of each stage's B half, so
+// the transform warps only handle A; idle otherwise).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -41,7 +43,7 @@ using namespace sm100;
 
 constexpr int BMC = 128;  // rows per CTA (pair tile = 256)
 constexpr int BK = 32;    // fp32 per 128-byte swizzle row
-constexpr int NTHREADS = 320;
+constexpr int NTHREADS = 448;  // 14 warps: see the role list in the header comment
 constexpr int A_TILE = BMC * BK * 4;  // 16 KB
 
 struct DevArgs {
@@ -175,7 +177,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&ld_full[s], 1);
-      mbar_init(&full[s], RELAY ? 2 * 128 : 1);
+      // RELAY: both CTAs' 128 transform threads (+ 128 B-split threads each when they run) arrive
+      mbar_init(&full[s], RELAY ? 2 * 128 * ((THREE_X && !BRES && args.b_mn) ? 2 : 1) : 1);
       mbar_init(&empty[s], 1);
     }
     for (int l = 0; l < SL; ++l) mbar_init(&lo_empty[l], 1);
@@ -477,7 +480,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                                        v.w - tf32_hi(v.w)));
         }
       }
-      if (!BRES && bmn_lo) split_b(b_hi(s), b_lo(s), C_::BHALF);
       fence_proxy_async_smem();
       mbar_arrive_remote(full_leader + (uint32_t)(s * sizeof(uint64_t)));
     };
@@ -585,6 +587,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       for (int i = 0; i < SL; ++i, ++it) {
         const uint32_t ul = it / SL;
         if (ul > 0) mbar_wait(&lo_empty[it % SL], (ul - 1) & 1);
+      }
+    }
+  } else if (warp >= 10) {
+    // ============================ B-lo split (warps 10-13) ============================
+    if (THREE_X && !BRES && args.b_mn) {
+      const int t2 = threadIdx.x - 320;
+      const uint32_t full_leader = mapa(smem_u32(full), 0);
+      uint32_t it = 0;
+      for (int tt, jj = 0; (tt = tile_at(args, cid, ncl, jj)) >= 0; ++jj) {
+        const Tile tl = decode(args, tt);
+        for (int kb = tl.kb0; kb < tl.kb1; ++kb, ++it) {
+          const int s = it % S;
+          mbar_wait(&ld_full[s], (it / S) & 1);
+          const uint32_t h = smem_u32(b_hi(s)), l = smem_u32(b_lo(s));
+          // lo = b - trunc_tf32(b), elementwise: the swizzled MN-major layout carries over
+#pragma unroll 4
+          for (int i = t2 * 16; i < C_::BHALF; i += 128 * 16) {
+            const float4 v = lds128(h + (uint32_t)i);
+            sts128(l + (uint32_t)i, make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z),
+                                                v.w - tf32_hi(v.w)));
+          }
+          fence_proxy_async_smem();
+          mbar_arrive_remote(full_leader + (uint32_t)(s * sizeof(uint64_t)));
+        }
       }
     }
   } else {
