@@ -183,3 +183,11 @@ def test_pool_validation_errors_before_any_launch(C):
     with pytest.raises(RuntimeError) as ei:
         C.pool2d_forward(P(1, 4, 4, 1, 2, 2), 18, 16, stream=0)
     assert "ALIGNMENT" in str(ei.value)
+
+
+def test_autotune_flush_registration(C):
+    with pytest.raises(RuntimeError) as ei:
+        C.conv2d_set_autotune_flush(4096, 0)   # a buffer of 0 bytes
+    assert "INVALID_PARAMS" in str(ei.value)
+    C.conv2d_set_autotune_flush(4096, 1 << 20)  # registration only: never dereferenced on the host
+    C.conv2d_set_autotune_flush(None)

@@ -7,7 +7,7 @@ algorithm, plus the fraction of each layer's own roofline).
 import json
 import sys
 
-ALGOS = ["direct", "tiled", "implicit_gemm", "winograd_f2x2_3x3", "matmul_1x1", "auto"]
+ALGOS = ["direct", "tiled", "implicit_gemm", "winograd_f2x2_3x3", "winograd_f4x4_3x3", "matmul_1x1", "auto"]
 
 
 def main():
