@@ -92,8 +92,10 @@ __global__ void wino_filter_kernel(const float* __restrict__ w, int C, int F, in
   constexpr int AL = MT + 2;
   const int64_t total = cpad * fpad;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int f = (int)(i % fpad);
-    const int c = (int)(i / fpad);
+    // c fastest: the 36 (72 with lo) K-major Ut[xi][f][c] stores of a warp are contiguous; only the 9
+    // HWCF reads per thread are strided (by F)
+    const int c = (int)(i % cpad);
+    const int f = (int)(i / cpad);
     float u[AL][AL];
     if (c < C && f < F) {
       float t[AL][3];  // G g, column by column
@@ -130,89 +132,132 @@ __global__ void wino_filter_kernel(const float* __restrict__ w, int C, int F, in
 }
 
 // V[xi][t][c] (row stride cpad), t = (n, th, tw); V = B^T d B over the ALPHA x ALPHA input tile at
-// (MT*th - PT, MT*tw - PL) (tiles overlap by 2)
-template <int MT>
+// (MT*th - PT, MT*tw - PL) (tiles overlap by 2).  VEC: four consecutive channels per thread (float4 loads
+// and stores; C % 4 == 0), channel groups fastest so a warp's accesses are contiguous.
+template <int MT, bool VEC>
 __global__ void wino_input_kernel(const float* __restrict__ x, int H, int W, int C, int TH, int TW, int PT, int PL,
                                   int64_t T, int64_t cpad, float* __restrict__ V, int round_rna) {
   pdl_trigger();
   pdl_wait();
   constexpr int AL = MT + 2;
-  const int64_t total = T * cpad;
+  constexpr int NV = VEC ? 4 : 1;
+  const int64_t cg_n = cpad / NV;
+  const int64_t total = T * cg_n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % cpad);
-    const int64_t t = i / cpad;
+    const int c0 = (int)(i % cg_n) * NV;
+    const int64_t t = i / cg_n;
     const int tw = (int)(t % TW);
     const int th = (int)((t / TW) % TH);
     const int64_t n = t / ((int64_t)TW * TH);
-    float d[AL][AL];
+    float d[NV][AL][AL];
     const int h0 = MT * th - PT, w0 = MT * tw - PL;
 #pragma unroll
     for (int a = 0; a < AL; ++a)
 #pragma unroll
       for (int b = 0; b < AL; ++b) {
         const int ih = h0 + a, iw = w0 + b;
-        d[a][b] = (c < C && ih >= 0 && ih < H && iw >= 0 && iw < W) ? x[((n * H + ih) * W + iw) * C + c] : 0.f;
+        const bool in = c0 < C && ih >= 0 && ih < H && iw >= 0 && iw < W;
+        const float* src = x + ((n * H + ih) * W + iw) * C + c0;
+        if constexpr (VEC) {
+          const float4 v = in ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0.f, 0.f, 0.f, 0.f);
+          d[0][a][b] = v.x;
+          d[1][a][b] = v.y;
+          d[2][a][b] = v.z;
+          d[3][a][b] = v.w;
+        } else {
+          d[0][a][b] = in ? src[0] : 0.f;
+        }
       }
-    float q[AL][AL];  // B^T d, column by column
+    float out[NV][AL][AL];
 #pragma unroll
-    for (int b = 0; b < AL; ++b) {
-      float col[AL], out[AL];
-#pragma unroll
-      for (int a = 0; a < AL; ++a) col[a] = d[a][b];
-      bT<MT>(col, out);
-#pragma unroll
-      for (int a = 0; a < AL; ++a) q[a][b] = out[a];
-    }
-#pragma unroll
-    for (int a = 0; a < AL; ++a) {  // (B^T d) B
-      float vv[AL];
-      bT<MT>(q[a], vv);
+    for (int e = 0; e < NV; ++e) {
+      float q[AL][AL];  // B^T d, column by column
 #pragma unroll
       for (int b = 0; b < AL; ++b) {
-        const float v = round_rna ? tf32_rna(vv[b]) : vv[b];
-        V[((int64_t)(a * AL + b) * T + t) * cpad + c] = v;
+        float col[AL], o[AL];
+#pragma unroll
+        for (int a = 0; a < AL; ++a) col[a] = d[e][a][b];
+        bT<MT>(col, o);
+#pragma unroll
+        for (int a = 0; a < AL; ++a) q[a][b] = o[a];
       }
+#pragma unroll
+      for (int a = 0; a < AL; ++a) bT<MT>(q[a], out[e][a]);  // (B^T d) B
     }
+#pragma unroll
+    for (int a = 0; a < AL; ++a)
+#pragma unroll
+      for (int b = 0; b < AL; ++b) {
+        float* dst = V + ((int64_t)(a * AL + b) * T + t) * cpad + c0;
+        if constexpr (VEC) {
+          float4 v = make_float4(out[0][a][b], out[1][a][b], out[2][a][b], out[3][a][b]);
+          if (round_rna) v = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+          *reinterpret_cast<float4*>(dst) = v;
+        } else {
+          dst[0] = round_rna ? tf32_rna(out[0][a][b]) : out[0][a][b];
+        }
+      }
   }
 }
 
-// Y tile (MT x MT) = A^T M A, M[xi][t][f] (row stride ldm)
-template <int MT>
+// Y tile (MT x MT) = A^T M A, M[xi][t][f] (row stride ldm).  VEC: four consecutive features per thread
+// (float4; F % 4 == 0), feature groups fastest.
+template <int MT, bool VEC>
 __global__ void wino_output_kernel(const float* __restrict__ Mw, int64_t T, int64_t ldm, int F, int HO, int WO,
                                    int TH, int TW, float* __restrict__ y) {
   pdl_trigger();
   pdl_wait();
   constexpr int AL = MT + 2;
-  const int64_t total = T * F;
+  constexpr int NV = VEC ? 4 : 1;
+  const int64_t fg_n = F / NV;
+  const int64_t total = T * fg_n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int f = (int)(i % F);
-    const int64_t t = i / F;
-    float m[AL][AL];
+    const int f0 = (int)(i % fg_n) * NV;
+    const int64_t t = i / fg_n;
+    float m[NV][AL][AL];
 #pragma unroll
-    for (int xi = 0; xi < AL * AL; ++xi) m[xi / AL][xi % AL] = Mw[((int64_t)xi * T + t) * ldm + f];
-    float r[MT][AL];  // A^T M, column by column
-#pragma unroll
-    for (int b = 0; b < AL; ++b) {
-      float col[AL], out[MT];
-#pragma unroll
-      for (int a = 0; a < AL; ++a) col[a] = m[a][b];
-      aT<MT>(col, out);
-#pragma unroll
-      for (int a = 0; a < MT; ++a) r[a][b] = out[a];
+    for (int xi = 0; xi < AL * AL; ++xi) {
+      const float* src = Mw + ((int64_t)xi * T + t) * ldm + f0;
+      if constexpr (VEC) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(src));
+        m[0][xi / AL][xi % AL] = v.x;
+        m[1][xi / AL][xi % AL] = v.y;
+        m[2][xi / AL][xi % AL] = v.z;
+        m[3][xi / AL][xi % AL] = v.w;
+      } else {
+        m[0][xi / AL][xi % AL] = src[0];
+      }
     }
     const int tw = (int)(t % TW);
     const int th = (int)((t / TW) % TH);
     const int64_t n = t / ((int64_t)TW * TH);
+    float yy[NV][MT][MT];
+#pragma unroll
+    for (int e = 0; e < NV; ++e) {
+      float r[MT][AL];  // A^T M, column by column
+#pragma unroll
+      for (int b = 0; b < AL; ++b) {
+        float col[AL], o[MT];
+#pragma unroll
+        for (int a = 0; a < AL; ++a) col[a] = m[e][a][b];
+        aT<MT>(col, o);
+#pragma unroll
+        for (int a = 0; a < MT; ++a) r[a][b] = o[a];
+      }
+#pragma unroll
+      for (int a = 0; a < MT; ++a) aT<MT>(r[a], yy[e][a]);  // (A^T M) A
+    }
 #pragma unroll
     for (int a = 0; a < MT; ++a) {
-      float yy[MT];
-      aT<MT>(r[a], yy);  // (A^T M) A
       const int ho = MT * th + a;
       if (ho >= HO) continue;
 #pragma unroll
       for (int b = 0; b < MT; ++b) {
         const int wo = MT * tw + b;
-        if (wo < WO) y[((n * HO + ho) * WO + wo) * F + f] = yy[b];
+        if (wo >= WO) continue;
+        float* dst = y + ((n * HO + ho) * WO + wo) * F + f0;
+        if constexpr (VEC) *reinterpret_cast<float4*>(dst) = make_float4(yy[0][a][b], yy[1][a][b], yy[2][a][b], yy[3][a][b]);
+        else dst[0] = yy[0][a][b];
       }
     }
   }
@@ -278,12 +323,16 @@ cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const flo
   float* partial = w.splits > 1 ? reinterpret_cast<float*>(b) : nullptr;
 
   auto kf = mt == 2 ? wino_filter_kernel<2> : wino_filter_kernel<4>;
-  auto ki = mt == 2 ? wino_input_kernel<2> : wino_input_kernel<4>;
-  auto ko = mt == 2 ? wino_output_kernel<2> : wino_output_kernel<4>;
+  const bool vin = p.C % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;  // cpad % 32 == 0 always
+  const bool vout = p.F % 4 == 0 && w.ldm % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  auto ki = mt == 2 ? (vin ? wino_input_kernel<2, true> : wino_input_kernel<2, false>)
+                    : (vin ? wino_input_kernel<4, true> : wino_input_kernel<4, false>);
+  auto ko = mt == 2 ? (vout ? wino_output_kernel<2, true> : wino_output_kernel<2, false>)
+                    : (vout ? wino_output_kernel<4, true> : wino_output_kernel<4, false>);
   cudaError_t e = launch_k(kf, dim3(grid_for(w.cpad * w.fpad)), dim3(256), 0, s, filt, p.C, p.F, w.cpad, w.fpad,
                            ut_hi, ut_lo, w.three_x ? 0 : 1);
   if (e != cudaSuccess) return e;
-  e = launch_k(ki, dim3(grid_for(w.T * w.cpad)), dim3(256), 0, s, in, p.H, p.W, p.C, w.TH, w.TW, p.pad_top,
+  e = launch_k(ki, dim3(grid_for(w.T * w.cpad / (vin ? 4 : 1))), dim3(256), 0, s, in, p.H, p.W, p.C, w.TH, w.TW, p.pad_top,
                p.pad_left, w.T, w.cpad, V, w.three_x ? 0 : 1);
   if (e != cudaSuccess) return e;
   Gemm2Args g{};
@@ -307,7 +356,7 @@ cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const flo
   g.block_n = w.block_n;
   e = launch_gemm2(p, g, s);
   if (e != cudaSuccess) return e;
-  return launch_k(ko, dim3(grid_for(w.T * p.F)), dim3(256), 0, s, Mw, w.T, w.ldm, p.F, p.HO, p.WO, w.TH, w.TW, out);
+  return launch_k(ko, dim3(grid_for(w.T * p.F / (vout ? 4 : 1))), dim3(256), 0, s, Mw, w.T, w.ldm, p.F, p.HO, p.WO, w.TH, w.TW, out);
 }
 
 }  // namespace conv2d
