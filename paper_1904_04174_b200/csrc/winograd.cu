@@ -83,39 +83,41 @@ template <int MT> __device__ __forceinline__ void gT(const float* g, float* u) {
 template <int MT> __device__ __forceinline__ void bT(const float* d, float* v) { if (MT == 2) bt2(d, v); else bt4(d, v); }
 template <int MT> __device__ __forceinline__ void aT(const float* m, float* y) { if (MT == 2) at2(m, y); else at4(m, y); }
 
-// U_xi stored K-major per xi: Ut[xi][f][c], Fpad rows x Cpad cols; U = G g G^T (ALPHA x ALPHA)
+// U_xi stored K-major per xi: Ut[xi][f][c], Fpad rows x Cpad cols; U = G g G^T (ALPHA x ALPHA).
+// One block per 32 (c) x 8 (f) tile (one (c, f) per thread): the nine HWCF taps are read f-fastest into
+// smem, then each thread transforms its (c, f) with c fastest so the Ut stores are coalesced too.
 template <int MT>
-__global__ void wino_filter_kernel(const float* __restrict__ w, int C, int F, int64_t cpad, int64_t fpad,
-                                   float* __restrict__ ut_hi, float* __restrict__ ut_lo, int mode /*0 3x,1 tf32*/) {
+__global__ void __launch_bounds__(256) wino_filter_kernel(const float* __restrict__ w, int C, int F, int64_t cpad,
+                                                          int64_t fpad, float* __restrict__ ut_hi,
+                                                          float* __restrict__ ut_lo, int mode /*0 3x,1 tf32*/) {
   pdl_trigger();
   pdl_wait();
   constexpr int AL = MT + 2;
-  const int64_t total = cpad * fpad;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    // c fastest: the 36 (72 with lo) K-major Ut[xi][f][c] stores of a warp are contiguous; only the 9
-    // HWCF reads per thread are strided (by F)
-    const int c = (int)(i % cpad);
-    const int f = (int)(i / cpad);
+  __shared__ float g_s[9][8][33];  // [tap][f][c]
+  const int c0 = blockIdx.x * 32, f0 = blockIdx.y * 8;
+  for (int q = threadIdx.x; q < 9 * 32 * 8; q += blockDim.x) {  // q = (tap, c, f), f fastest
+    const int fl = q % 8, cl = (q / 8) % 32, tap = q / 256;
+    const int c = c0 + cl, f = f0 + fl;
+    g_s[tap][fl][cl] = (c < C && f < F) ? w[((int64_t)tap * C + c) * F + f] : 0.f;
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < 32 * 8; q += blockDim.x) {  // q = (f, c), c fastest
+    const int cl = q % 32, fl = q / 32;
+    const int c = c0 + cl, f = f0 + fl;
+    if (c >= cpad || f >= fpad) continue;
     float u[AL][AL];
-    if (c < C && f < F) {
-      float t[AL][3];  // G g, column by column
+    float t[AL][3];  // G g, column by column
 #pragma unroll
-      for (int s = 0; s < 3; ++s) {
-        float col[3], out[AL];
+    for (int sc = 0; sc < 3; ++sc) {
+      float col[3], out[AL];
 #pragma unroll
-        for (int r = 0; r < 3; ++r) col[r] = w[((int64_t)(r * 3 + s) * C + c) * F + f];
-        gT<MT>(col, out);
+      for (int r = 0; r < 3; ++r) col[r] = g_s[r * 3 + sc][fl][cl];
+      gT<MT>(col, out);
 #pragma unroll
-        for (int r = 0; r < AL; ++r) t[r][s] = out[r];
-      }
-#pragma unroll
-      for (int r = 0; r < AL; ++r) gT<MT>(t[r], u[r]);  // (G g) G^T
-    } else {
-#pragma unroll
-      for (int r = 0; r < AL; ++r)
-#pragma unroll
-        for (int s = 0; s < AL; ++s) u[r][s] = 0.f;
+      for (int r = 0; r < AL; ++r) t[r][sc] = out[r];
     }
+#pragma unroll
+    for (int r = 0; r < AL; ++r) gT<MT>(t[r], u[r]);  // (G g) G^T
 #pragma unroll
     for (int xi = 0; xi < AL * AL; ++xi) {
       const float v = u[xi / AL][xi % AL];
@@ -134,13 +136,12 @@ __global__ void wino_filter_kernel(const float* __restrict__ w, int C, int F, in
 // V[xi][t][c] (row stride cpad), t = (n, th, tw); V = B^T d B over the ALPHA x ALPHA input tile at
 // (MT*th - PT, MT*tw - PL) (tiles overlap by 2).  VEC: four consecutive channels per thread (float4 loads
 // and stores; C % 4 == 0), channel groups fastest so a warp's accesses are contiguous.
-template <int MT, bool VEC>
+template <int MT, int NV>
 __global__ void wino_input_kernel(const float* __restrict__ x, int H, int W, int C, int TH, int TW, int PT, int PL,
                                   int64_t T, int64_t cpad, float* __restrict__ V, int round_rna) {
   pdl_trigger();
   pdl_wait();
   constexpr int AL = MT + 2;
-  constexpr int NV = VEC ? 4 : 1;
   const int64_t cg_n = cpad / NV;
   const int64_t total = T * cg_n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -158,12 +159,16 @@ __global__ void wino_input_kernel(const float* __restrict__ x, int H, int W, int
         const int ih = h0 + a, iw = w0 + b;
         const bool in = c0 < C && ih >= 0 && ih < H && iw >= 0 && iw < W;
         const float* src = x + ((n * H + ih) * W + iw) * C + c0;
-        if constexpr (VEC) {
+        if constexpr (NV == 4) {
           const float4 v = in ? __ldg(reinterpret_cast<const float4*>(src)) : make_float4(0.f, 0.f, 0.f, 0.f);
           d[0][a][b] = v.x;
           d[1][a][b] = v.y;
           d[2][a][b] = v.z;
           d[3][a][b] = v.w;
+        } else if constexpr (NV == 2) {
+          const float2 v = in ? __ldg(reinterpret_cast<const float2*>(src)) : make_float2(0.f, 0.f);
+          d[0][a][b] = v.x;
+          d[1][a][b] = v.y;
         } else {
           d[0][a][b] = in ? src[0] : 0.f;
         }
@@ -189,10 +194,14 @@ __global__ void wino_input_kernel(const float* __restrict__ x, int H, int W, int
 #pragma unroll
       for (int b = 0; b < AL; ++b) {
         float* dst = V + ((int64_t)(a * AL + b) * T + t) * cpad + c0;
-        if constexpr (VEC) {
+        if constexpr (NV == 4) {
           float4 v = make_float4(out[0][a][b], out[1][a][b], out[2][a][b], out[3][a][b]);
           if (round_rna) v = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
           *reinterpret_cast<float4*>(dst) = v;
+        } else if constexpr (NV == 2) {
+          float2 v = make_float2(out[0][a][b], out[1][a][b]);
+          if (round_rna) v = make_float2(tf32_rna(v.x), tf32_rna(v.y));
+          *reinterpret_cast<float2*>(dst) = v;
         } else {
           dst[0] = round_rna ? tf32_rna(out[0][a][b]) : out[0][a][b];
         }
@@ -323,16 +332,19 @@ cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const flo
   float* partial = w.splits > 1 ? reinterpret_cast<float*>(b) : nullptr;
 
   auto kf = mt == 2 ? wino_filter_kernel<2> : wino_filter_kernel<4>;
-  const bool vin = p.C % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;  // cpad % 32 == 0 always
+  // input transform: F(2x2) moves 4 channels per thread; F(4x4) 2 (its 6x6 tiles would otherwise need ~190
+  // registers per thread and run at 12% occupancy)
+  const int nvin = (p.C % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) ? (mt == 2 ? 4 : 2)
+                   : (p.C % 2 == 0 && (reinterpret_cast<uintptr_t>(in) & 7) == 0) ? 2 : 1;  // cpad % 32 == 0
   const bool vout = p.F % 4 == 0 && w.ldm % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-  auto ki = mt == 2 ? (vin ? wino_input_kernel<2, true> : wino_input_kernel<2, false>)
-                    : (vin ? wino_input_kernel<4, true> : wino_input_kernel<4, false>);
+  auto ki = mt == 2 ? (nvin == 4 ? wino_input_kernel<2, 4> : nvin == 2 ? wino_input_kernel<2, 2> : wino_input_kernel<2, 1>)
+                    : (nvin == 4 ? wino_input_kernel<4, 4> : nvin == 2 ? wino_input_kernel<4, 2> : wino_input_kernel<4, 1>);
   auto ko = mt == 2 ? (vout ? wino_output_kernel<2, true> : wino_output_kernel<2, false>)
                     : (vout ? wino_output_kernel<4, true> : wino_output_kernel<4, false>);
-  cudaError_t e = launch_k(kf, dim3(grid_for(w.cpad * w.fpad)), dim3(256), 0, s, filt, p.C, p.F, w.cpad, w.fpad,
-                           ut_hi, ut_lo, w.three_x ? 0 : 1);
+  cudaError_t e = launch_k(kf, dim3((unsigned)(w.cpad / 32), (unsigned)((w.fpad + 7) / 8)), dim3(256), 0, s, filt,
+                           p.C, p.F, w.cpad, w.fpad, ut_hi, ut_lo, w.three_x ? 0 : 1);
   if (e != cudaSuccess) return e;
-  e = launch_k(ki, dim3(grid_for(w.T * w.cpad / (vin ? 4 : 1))), dim3(256), 0, s, in, p.H, p.W, p.C, w.TH, w.TW, p.pad_top,
+  e = launch_k(ki, dim3(grid_for(w.T * w.cpad / nvin)), dim3(256), 0, s, in, p.H, p.W, p.C, w.TH, w.TW, p.pad_top,
                p.pad_left, w.T, w.cpad, V, w.three_x ? 0 : 1);
   if (e != cudaSuccess) return e;
   Gemm2Args g{};
