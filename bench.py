@@ -430,6 +430,7 @@ def main():
             traffic = round(tj["gemm_dram_bytes"] / tj["gemm_launches"] / 1e6, 2)
             traffic_src = (f"MB per GEMM-core launch (gemm2sm / halo), ncu dram__bytes_read.sum+write.sum over one "
                            f"timed step ({tj['gemm_launches']} launches; profiles/round1_ncu.md)")
+    n_wino = sum(1 for cv, _ in grp if cv["algo"] in (C.ALGO_WINOGRAD_F2X2_3X3, C.ALGO_WINOGRAD_F4X4_3X3))
     roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(useful_peak, 1), "unit": "TFLOP/s",
             "frac": round(ach / useful_peak, 4), "traffic": traffic,
             "traffic_unit": traffic_src, "algorithmic_mb_per_launch": round(g_bytes / len(grp) / 1e6, 2),
@@ -437,6 +438,10 @@ def main():
                       f"matmul_1x1|winograd]: {len(grp)} of {len(convs)} convs, {100 * share:.1f}% of step",
             "timing": "CUDA events at the timed steps' boundaries (launching stream) x the group's share of "
                       "per-conv event times from K instrumented replays after the timed region",
+            "flop_accounting": f"direct-convolution flops 2*N*Ho*Wo*K^2*C*F for every conv (DESIGN.md reading R8, the "
+                               f"paper's Fig.-1 methodology); {n_wino} of {len(grp)} convs run Winograd, which executes "
+                               f"2.25x (F2x2) / 4x (F4x4) fewer multiplies, so the group's direct-normalised rate is "
+                               f"not a pure tensor-pipe utilisation",
             "peak_source": f"{peak_src} bf16 burst {peaks['bf16_tflops']} TF/s /2 (TF32)"
                            + (" /3 (3xTF32 useful flops)" if math == C.MATH_FP32 else "")}
     # whole-step roofline: sum over convs of max(flops/peak, bytes/hbm)
