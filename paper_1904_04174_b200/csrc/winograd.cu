@@ -87,14 +87,12 @@ template <int MT> __device__ __forceinline__ void aT(const float* m, float* y) {
 // One block per 32 (c) x 8 (f) tile (one (c, f) per thread): the nine HWCF taps are read f-fastest into
 // smem, then each thread transforms its (c, f) with c fastest so the Ut stores are coalesced too.
 template <int MT>
-__global__ void __launch_bounds__(256) wino_filter_kernel(const float* __restrict__ w, int C, int F, int64_t cpad,
-                                                          int64_t fpad, float* __restrict__ ut_hi,
-                                                          float* __restrict__ ut_lo, int mode /*0 3x,1 tf32*/) {
-  pdl_trigger();
-  pdl_wait();
+__device__ __forceinline__ void wino_filter_tile(const float* __restrict__ w, int C, int F, int64_t cpad, int64_t fpad,
+                                                 float* __restrict__ ut_hi, float* __restrict__ ut_lo, int mode,
+                                                 int bx, int by) {
   constexpr int AL = MT + 2;
   __shared__ float g_s[9][8][33];  // [tap][f][c]
-  const int c0 = blockIdx.x * 32, f0 = blockIdx.y * 8;
+  const int c0 = bx * 32, f0 = by * 8;
   for (int q = threadIdx.x; q < 9 * 32 * 8; q += blockDim.x) {  // q = (tap, c, f), f fastest
     const int fl = q % 8, cl = (q / 8) % 32, tap = q / 256;
     const int c = c0 + cl, f = f0 + fl;
@@ -137,14 +135,13 @@ __global__ void __launch_bounds__(256) wino_filter_kernel(const float* __restric
 // (MT*th - PT, MT*tw - PL) (tiles overlap by 2).  VEC: four consecutive channels per thread (float4 loads
 // and stores; C % 4 == 0), channel groups fastest so a warp's accesses are contiguous.
 template <int MT, int NV>
-__global__ void wino_input_kernel(const float* __restrict__ x, int H, int W, int C, int TH, int TW, int PT, int PL,
-                                  int64_t T, int64_t cpad, float* __restrict__ V, int round_rna) {
-  pdl_trigger();
-  pdl_wait();
+__device__ __forceinline__ void wino_input_body(const float* __restrict__ x, int H, int W, int C, int TH, int TW,
+                                                int PT, int PL, int64_t T, int64_t cpad, float* __restrict__ V,
+                                                int round_rna, int64_t blk, int64_t nblk) {
   constexpr int AL = MT + 2;
   const int64_t cg_n = cpad / NV;
   const int64_t total = T * cg_n;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i = blk * blockDim.x + threadIdx.x; i < total; i += nblk * blockDim.x) {
     const int c0 = (int)(i % cg_n) * NV;
     const int64_t t = i / cg_n;
     const int tw = (int)(t % TW);
@@ -207,6 +204,25 @@ __global__ void wino_input_kernel(const float* __restrict__ x, int H, int W, int
         }
       }
   }
+}
+
+// One launch for both operand transforms (they are independent): blocks [0, nfx*nfy) transform 32x8
+// filter tiles, the rest run the input transform grid-stride -- one kernel boundary fewer per Winograd
+// conv, and the filter work overlaps the input transform.
+template <int MT, int NV>
+__global__ void __launch_bounds__(256) wino_prep_kernel(const float* __restrict__ w, int C, int F, int64_t cpad,
+                                                        int64_t fpad, float* __restrict__ ut_hi,
+                                                        float* __restrict__ ut_lo, int mode, int nfx, int nfy,
+                                                        const float* __restrict__ x, int H, int W, int TH, int TW,
+                                                        int PT, int PL, int64_t T, float* __restrict__ V) {
+  pdl_trigger();
+  pdl_wait();
+  const int nf = nfx * nfy;
+  if ((int)blockIdx.x < nf)
+    wino_filter_tile<MT>(w, C, F, cpad, fpad, ut_hi, ut_lo, mode, (int)blockIdx.x % nfx, (int)blockIdx.x / nfx);
+  else
+    wino_input_body<MT, NV>(x, H, W, C, TH, TW, PT, PL, T, cpad, V, mode, (int64_t)blockIdx.x - nf,
+                            (int64_t)gridDim.x - nf);
 }
 
 // Y tile (MT x MT) = A^T M A, M[xi][t][f] (row stride ldm).  VEC: four consecutive features per thread
@@ -312,7 +328,7 @@ unsigned grid_for(int64_t total) {
 }  // namespace
 
 size_t winograd_workspace(const Problem& p, int mt) { return make_wplan(p, mt).total; }
-int winograd_launches(const Problem& p, int mt) { return 4 + (make_wplan(p, mt).splits > 1 ? 1 : 0); }
+int winograd_launches(const Problem& p, int mt) { return 3 + (make_wplan(p, mt).splits > 1 ? 1 : 0); }
 
 cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const float* filt, float* out, void* ws,
                             cudaStream_t s) {
@@ -331,21 +347,19 @@ cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const flo
   b += w.m_bytes;
   float* partial = w.splits > 1 ? reinterpret_cast<float*>(b) : nullptr;
 
-  auto kf = mt == 2 ? wino_filter_kernel<2> : wino_filter_kernel<4>;
   // input transform: F(2x2) moves 4 channels per thread; F(4x4) 2 (its 6x6 tiles would otherwise need ~190
   // registers per thread and run at 12% occupancy)
   const int nvin = (p.C % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) ? (mt == 2 ? 4 : 2)
                    : (p.C % 2 == 0 && (reinterpret_cast<uintptr_t>(in) & 7) == 0) ? 2 : 1;  // cpad % 32 == 0
   const bool vout = p.F % 4 == 0 && w.ldm % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-  auto ki = mt == 2 ? (nvin == 4 ? wino_input_kernel<2, 4> : nvin == 2 ? wino_input_kernel<2, 2> : wino_input_kernel<2, 1>)
-                    : (nvin == 4 ? wino_input_kernel<4, 4> : nvin == 2 ? wino_input_kernel<4, 2> : wino_input_kernel<4, 1>);
+  auto kp = mt == 2 ? (nvin == 4 ? wino_prep_kernel<2, 4> : nvin == 2 ? wino_prep_kernel<2, 2> : wino_prep_kernel<2, 1>)
+                    : (nvin == 4 ? wino_prep_kernel<4, 4> : nvin == 2 ? wino_prep_kernel<4, 2> : wino_prep_kernel<4, 1>);
   auto ko = mt == 2 ? (vout ? wino_output_kernel<2, true> : wino_output_kernel<2, false>)
                     : (vout ? wino_output_kernel<4, true> : wino_output_kernel<4, false>);
-  cudaError_t e = launch_k(kf, dim3((unsigned)(w.cpad / 32), (unsigned)((w.fpad + 7) / 8)), dim3(256), 0, s, filt,
-                           p.C, p.F, w.cpad, w.fpad, ut_hi, ut_lo, w.three_x ? 0 : 1);
-  if (e != cudaSuccess) return e;
-  e = launch_k(ki, dim3(grid_for(w.T * w.cpad / nvin)), dim3(256), 0, s, in, p.H, p.W, p.C, w.TH, w.TW, p.pad_top,
-               p.pad_left, w.T, w.cpad, V, w.three_x ? 0 : 1);
+  const int nfx = (int)(w.cpad / 32), nfy = (int)((w.fpad + 7) / 8);
+  cudaError_t e = launch_k(kp, dim3((unsigned)(nfx * nfy) + grid_for(w.T * w.cpad / nvin)), dim3(256), 0, s, filt, p.C,
+                           p.F, w.cpad, w.fpad, ut_hi, ut_lo, w.three_x ? 0 : 1, nfx, nfy, in, p.H, p.W, w.TH, w.TW,
+                           p.pad_top, p.pad_left, w.T, V);
   if (e != cudaSuccess) return e;
   Gemm2Args g{};
   g.a_mode = A_DENSE;
