@@ -59,6 +59,17 @@ struct HArgs {
   // GS2D raw mode: tmX boxes are raw input patches (RAW_ROWS rows x 32 pixels x rc channels of x, origin
   // (2*ho0 - rpt, 2*wo0 - rpl)) and the transform warps build the swizzled s2d halo from them
   int raw, rc, rpt, rpl;
+  // GS2D: the K=8 steps that touch a real (tap, slot), in B's k order: code = tap*2 + half (half = slots
+  // 8h..8h+7 of the tap's 16); kbu = ceil(steps / 4) k-blocks (all-padding steps are never issued -- with
+  // C = 3 the second half of the a = 3 taps of a 7x7 stem; the list is padded with zero-B steps)
+  // per k-block kb: the four steps' A-view offsets from the halo base, in 16-byte descriptor units (u16 x 4)
+  uint64_t soff[8];
+  int kbu;
+};
+
+struct S2DSteps {
+  uint8_t code[32];  // tap*2 + half per issued K=8 step
+  int n;             // issued (non-padding) steps
 };
 
 constexpr int RAW_ROWS = 2 * (TH + 3);  // 38 input rows behind a 19-row s2d halo
@@ -142,7 +153,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
-  constexpr int KBU = G_::KB_PER_UNIT;
+  const int KBU = GEOM == GS2D ? args.kbu : G_::KB_PER_UNIT;
   pdl_trigger();  // launch.cuh
   if (threadIdx.x == 0 && args.trace) args.trace[blockIdx.x * 8 + 0] = globaltimer_ns();
 
@@ -255,6 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       }
       for (int t = cid; t < args.total; t += ncl, ++ai) {
         const int acc = ai & 1;
+        uint64_t soff_next = GEOM == GS2D ? args.soff[0] : 0;  // GS2D: next k-block's view offsets, a step ahead
         if (ai >= 2) mbar_wait(&tmem_empty[acc], ((ai >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * C_::ACC);
@@ -263,6 +275,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           mbar_wait(&h_full[h], (hit / HS) & 1);
           tc_fence_after();
           for (int kb = 0; kb < KBU; ++kb, ++bit) {
+            const uint64_t soff = soff_next;
+            if constexpr (GEOM == GS2D) soff_next = args.soff[kb + 1 < 8 ? kb + 1 : 7];
             const int s = C_::BRES ? kb : (int)(bit % S);
             if (!C_::BRES) {
               mbar_wait(&b_full[s], (bit / S) & 1);
@@ -278,23 +292,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               return GEOM == GS2D ? umma_desc_sw64_kmajor_sbo(a, HWD * G_::ROWB)
                                   : umma_desc_sw128_kmajor_sbo(a, HWD * G_::ROWB, 0u);
             };
-            const int tap0 = GEOM == GS2D ? 2 * kb : kb;
+            const int tap0 = GEOM == GS2D ? 0 : kb;
             const uint64_t dah0 = view(smem_u32(halo_hi(h)), tap0);
             const uint64_t dal0 = THREE_X ? view(smem_u32(halo_lo(h)), tap0) : 0;
-            const uint64_t dah1 = GEOM == GS2D ? view(smem_u32(halo_hi(h)), tap0 + 1) : dah0;
-            const uint64_t dal1 = (GEOM == GS2D && THREE_X) ? view(smem_u32(halo_lo(h)), tap0 + 1) : dal0;
             const uint64_t dbx = umma_desc_sw128_kmajor(smem_u32(b_x(s)));
             const uint64_t dbz = C_::CONCAT ? umma_desc_sw128_kmajor(smem_u32(b_z(s))) : 0;
             const uint64_t dbl = (THREE_X && !C_::CONCAT) ? umma_desc_sw128_kmajor(smem_u32(b_lo(s))) : 0;
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
               const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);  // B: 32 bytes per K=8 step
-              // A: G3X3 steps through the tap's 128-byte row; GS2D takes steps 0-1 from tap 2kb's 64-byte
-              // row and steps 2-3 from tap 2kb+1's
-              const bool second = GEOM == GS2D && k >= 2;
-              const uint64_t adv_a = GEOM == GS2D ? (uint64_t)(((k & 1) * 32) >> 4) : adv;
-              const uint64_t dah = (second ? dah1 : dah0) + adv_a;
-              const uint64_t dal = (second ? dal1 : dal0) + adv_a;
+              // A: G3X3 steps through the tap's 128-byte row; GS2D step 4kb+k is (tap, half) from the step
+              // table: the tap's view plus 32 bytes for the second 8 slots (uniform arithmetic, no branch)
+              uint64_t dah, dal;
+              if constexpr (GEOM == GS2D) {
+                const uint64_t off = (soff >> (16 * k)) & 0xFFFFu;
+                dah = dah0 + off;
+                dal = dal0 + off;
+              } else {
+                dah = dah0 + adv;
+                dal = dal0 + adv;
+              }
               const uint32_t accum = (cb > 0 || kb > 0 || k > 0) ? 1u : 0u;
               if (THREE_X && !C_::CONCAT) {
                 mma_tf32_2sm_warp(d, dal, dbx + adv, idesc, accum);
@@ -483,11 +500,22 @@ namespace {
 template <int GEOM>
 cudaError_t launch_halo_geo(const Problem& p, const float* x, int h, int w, int cx, int pt, int pl, int ncb,
                             const float* bt_hi, const float* bt_lo, int64_t kpad, int64_t npad, int block_n,
-                            float* out, cudaStream_t s, bool raw = false) {
+                            float* out, cudaStream_t s, bool raw = false, const void* s2d_steps = nullptr) {
   using G_ = Geo<GEOM>;
   const bool three_x = bt_lo != nullptr;
   HArgs a{};
   a.trace = gemm2_trace_record();
+  a.kbu = Geo<GEOM>::KB_PER_UNIT;
+  if (GEOM == GS2D && s2d_steps) {  // issued steps, in B's k order
+    const auto* st = static_cast<const S2DSteps*>(s2d_steps);
+    for (int i = 0; i < 32; ++i) {
+      const int tap = st->code[i] >> 1, half = st->code[i] & 1;
+      const uint64_t off = (uint64_t)(((tap / Geo<GS2D>::TAPW) * HWD + tap % Geo<GS2D>::TAPW) * Geo<GS2D>::ROWB +
+                                      half * 32) >> 4;
+      a.soff[i / 4] |= off << (16 * (i % 4));
+    }
+    a.kbu = (st->n + 3) / 4;
+  }
   a.N = p.N; a.H = h; a.W = w; a.HO = p.HO; a.WO = p.WO; a.PT = pt; a.PL = pl;
   a.ncb = ncb;
   a.tiles_w = (p.WO + TW - 1) / TW;
@@ -580,14 +608,21 @@ __global__ void s2d_input_kernel(const float* __restrict__ x, int N, int H, int 
 
 // Bt'[f][k] (npad x 256, K-major), k = (a*4 + e)*16 + (b*2 + d)*C + c  <-  w[2a+b][2e+d][c][f]; 3xTF32: hi/lo
 __global__ void s2d_filter_kernel(const float* __restrict__ w, int KH, int KW, int C, int F, int64_t npad,
-                                  float* __restrict__ bt_hi, float* __restrict__ bt_lo) {
+                                  float* __restrict__ bt_hi, float* __restrict__ bt_lo, const S2DSteps st) {
   pdl_trigger();
   pdl_wait();
   const int64_t total = npad * 256;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int k = (int)(i % 256);
     const int f = (int)(i / 256);
-    const int tap = k / 16, slot = k % 16;
+    // k = 8 * step + j: step -> (tap, half) from the table; steps past st.n are zero rows
+    const int step = k / 8, j = k % 8;
+    if (step >= st.n) {
+      bt_hi[i] = 0.f;
+      if (bt_lo) bt_lo[i] = 0.f;
+      continue;
+    }
+    const int tap = st.code[step] >> 1, slot = (st.code[step] & 1) * 8 + j;
     const int a = tap / 4, e = tap % 4;
     const int bd = C > 0 ? slot / C : 0, c = C > 0 ? slot % C : 0;
     const int r = 2 * a + (bd >> 1), sc = 2 * e + (bd & 1);
@@ -627,14 +662,30 @@ cudaError_t launch_gemm_s2d(const Problem& p, const float* in, const float* filt
   }
   float* xs = reinterpret_cast<float*>(w8);
   const int hs = p.HO + 3, wsd = p.WO + 3;
+  // the K=8 steps with any real (tap, slot) (slot = (b*2 + d)*C + c, tap = (a, e)): issued in this order
+  S2DSteps st{};
+  for (int code = 0; code < 32; ++code) {
+    const int tap = code >> 1, a_ = tap / 4, e_ = tap % 4;
+    bool any = false;
+    for (int slot = (code & 1) * 8; slot < (code & 1) * 8 + 8 && !any; ++slot) {
+      const int bd = slot / p.C;
+      any = bd < 4 && 2 * a_ + (bd >> 1) < p.KH && 2 * e_ + (bd & 1) < p.KW;
+    }
+    if (any) st.code[st.n++] = (uint8_t)code;
+  }
+  if (getenv("CONV2D_EXPERIMENT_ALL_STEPS")) {  // A/B: issue every step in natural order
+    st.n = 32;
+    for (int c = 0; c < 32; ++c) st.code[c] = (uint8_t)c;
+  }
+  for (int c = st.n; c < 32; ++c) st.code[c] = st.code[0];  // padding steps: any view, zero B rows
   // raw mode (C <= 3, 16-byte input rows): the GEMM builds s2d halos from raw input patches itself
   const bool raw = p.C <= 3 && ((int64_t)p.W * p.C) % 4 == 0 && getenv("CONV2D_S2D_PREPASS") == nullptr;
   if (raw) {
     int64_t fb = (npad * 256 + 255) / 256;
     cudaError_t e = launch_k(s2d_filter_kernel, dim3((unsigned)fb), dim3(256), 0, s, filt, p.KH, p.KW, p.C, p.F,
-                             npad, bt_hi, bt_lo);
+                             npad, bt_hi, bt_lo, st);
     if (e != cudaSuccess) return e;
-    return launch_halo_geo<GS2D>(p, in, hs, wsd, 16, 0, 0, 1, bt_hi, bt_lo, 256, npad, block_n, out, s, true);
+    return launch_halo_geo<GS2D>(p, in, hs, wsd, 16, 0, 0, 1, bt_hi, bt_lo, 256, npad, block_n, out, s, true, &st);
   }
   const int rows = p.N * hs;
   auto kin = p.C == 1 ? s2d_input_kernel<1> : p.C == 2 ? s2d_input_kernel<2> : p.C == 3 ? s2d_input_kernel<3>
@@ -645,9 +696,9 @@ cudaError_t launch_gemm_s2d(const Problem& p, const float* in, const float* filt
   if (e != cudaSuccess) return e;
   int64_t fb = (npad * 256 + 255) / 256;
   e = launch_k(s2d_filter_kernel, dim3((unsigned)fb), dim3(256), 0, s, filt, p.KH, p.KW, p.C, p.F, npad, bt_hi,
-               bt_lo);
+               bt_lo, st);
   if (e != cudaSuccess) return e;
-  return launch_halo_geo<GS2D>(p, xs, hs, wsd, 16, 0, 0, 1, bt_hi, bt_lo, 256, npad, block_n, out, s);
+  return launch_halo_geo<GS2D>(p, xs, hs, wsd, 16, 0, 0, 1, bt_hi, bt_lo, 256, npad, block_n, out, s, false, &st);
 }
 
 }  // namespace conv2d
