@@ -30,15 +30,16 @@ def main():
     rep, title = sys.argv[1], sys.argv[2]
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    h, units, v = rows[0], rows[1], rows[2]
-    name = v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
-    print(f"## {title}\n\n`{rep}` — kernel `{name[:160]}`\n\n| metric | value |\n|---|---:|")
-    vals = {}
-    for k, label in KEYS:
-        if k in h:
-            i = h.index(k)
-            vals[k] = (v[i], units[i])
-            print(f"| {label} (`{k}`) | {v[i]} {units[i]} |")
+    h, units = rows[0], rows[1]
+    print(f"## {title}\n\n`{rep}`\n")
+    for v in rows[2:]:  # one table per captured kernel
+        name = v[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+        print(f"kernel `{name[:160]}`\n\n| metric | value |\n|---|---:|")
+        for k, label in KEYS:
+            if k in h:
+                i = h.index(k)
+                print(f"| {label} (`{k}`) | {v[i]} {units[i]} |")
+        print()
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     srows = list(csv.reader(io.StringIO(src)))
