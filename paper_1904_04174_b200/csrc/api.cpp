@@ -223,7 +223,7 @@ conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int de
     // algorithm parameters: time every variant of the algorithm, keep its best
     const bool gemm_like = a == CONV2D_ALGO_IMPLICIT_GEMM || a == CONV2D_ALGO_MATMUL_1X1;
     const bool is_1x1 = a == CONV2D_ALGO_MATMUL_1X1;
-    int masks[16] = {0};
+    int masks[32] = {0};
     const int nvar = gemm_like ? igemm_variants(q, is_1x1, masks) : 1;
     double t_best = 1e300;
     int v_best = 0;
@@ -553,7 +553,7 @@ conv2d_status_t conv2d_load_selection(const char* path, int* loaded) {
       an = rhs.substr(0, slash);
       char* end = nullptr;
       const long v = strtol(rhs.c_str() + slash + 1, &end, 10);
-      if (!end || *end != '\0' || v < 0 || v > 15) {
+      if (!end || *end != '\0' || v < 0 || v > 31) {
         st = CONV2D_ERR_INVALID_PARAMS;
         why = "bad variant";
         break;

@@ -61,6 +61,11 @@ struct DevArgs {
   int64_t ldd, d_bstride;
   float* partial;
   int tma_store;  // 1: epilogue stages 32x32 chunks in smem and writes them with TMA stores
+  // remainder split (rs_splits >= 2): units [0, rs_first) are whole tiles; the remaining tiles of the
+  // partial last wave are cut into rs_splits K ranges each (units rs_first + i: tile rs_first + i / s, split
+  // i % s), stored to the partial planes via tmP and summed by rsplit_reduce_kernel afterwards
+  int rs_first, rs_splits;
+  alignas(64) CUtensorMap tmP;  // partial planes {N, M, s} (remainder split only)
   int bstat;  // B-stationary schedule (B-resident with several N tiles): pair p owns N tile p % nt
   int b_mn;  // 1: B read straight from the row-major K x F filter (MN-major operand; no filter_prep)
   unsigned long long* trace;  // debug (conv2d_debug_trace): TRACE_SLOTS globaltimer stamps per CTA, or null
@@ -99,10 +104,17 @@ struct Cfg {
 
 struct Tile {
   int mi, ni, bz, split, kb0, kb1;
+  bool part;  // remainder-split unit: accumulates K range [kb0, kb1) of its tile into partial plane `split`
 };
 
-__device__ __forceinline__ Tile decode(const DevArgs& a, int t) {
+__device__ __forceinline__ Tile decode(const DevArgs& a, int u) {
+  int t = u, rs = -1;
+  if (a.rs_splits > 1 && u >= a.rs_first) {
+    t = a.rs_first + (u - a.rs_first) / a.rs_splits;
+    rs = (u - a.rs_first) % a.rs_splits;
+  }
   Tile r;
+  r.part = rs >= 0;
   r.ni = t % a.nt;
   const int rest = t / a.nt;
   r.mi = rest % a.mt;
@@ -111,6 +123,11 @@ __device__ __forceinline__ Tile decode(const DevArgs& a, int t) {
   r.split = z % a.splits;
   r.kb0 = (int)((int64_t)r.split * a.nkb / a.splits);
   r.kb1 = (int)((int64_t)(r.split + 1) * a.nkb / a.splits);
+  if (rs >= 0) {
+    r.split = rs;
+    r.kb0 = (int)((int64_t)rs * a.nkb / a.rs_splits);
+    r.kb1 = (int)((int64_t)(rs + 1) * a.nkb / a.rs_splits);
+  }
   return r;
 }
 
@@ -623,6 +640,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const bool vec_ok = (args.ldd % 4) == 0;
     const uint32_t ebuf = smem_u32(epi_smem) + (uint32_t)(q * 2 * 4096);
     if (args.tma_store == 1 && lane == 0) tma_prefetch(&tmD);
+    if (args.rs_splits > 1 && lane == 0) tma_prefetch(&args.tmP);
     uint32_t ai = 0, chunk = 0;
     for (int t, jj = 0; (t = tile_at(args, cid, ncl, jj)) >= 0; ++jj, ++ai) {
       const Tile tl = decode(args, t);
@@ -695,6 +713,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             __syncwarp();
             if (lane == 0) {
               if (SPATIAL) tma_store_4d(&tmD, buf, n0 + c0, sw0, sh0, sn);
+              else if (tl.part) tma_store_3d(&args.tmP, buf, n0 + c0, (int)row0, tl.split);
               else tma_store_3d(&tmD, buf, n0 + c0, (int)row0, z);
               bulk_commit();
             }
@@ -988,9 +1007,13 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   a.nt = (int)((g.N + g.block_n - 1) / g.block_n);
   a.splits = g.splits;
   a.batch = g.batch;
-  const int64_t tiles = (int64_t)a.mt * a.nt * g.batch * g.splits;
+  int64_t tiles = (int64_t)a.mt * a.nt * g.batch * g.splits;
   if (tiles > 0x7FFFFFFF) return cudaErrorInvalidConfiguration;
   a.total_tiles = (int)tiles;
+  a.rs_first = a.rs_splits = 0;
+  const int rs = g.rsplit ? gemm2_rsplit_factor(tiles, a.nkb) : 0;
+  const bool rs_ok = rs >= 2 && g.splits == 1 && g.batch == 1 && g.partial && g.ldd % 4 == 0 &&
+                     g.a_mode != A_ROWSEG && g.a_mode != A_STEM;
   a.d = g.d; a.ldd = g.ldd; a.d_bstride = g.d_batch_stride; a.partial = g.partial;
   a.trace = gemm2_trace_record();
   a.b_mn = g.b_mn ? 1 : 0;
@@ -1054,6 +1077,21 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
     }
   }
   if (!ok) return cudaErrorInvalidValue;
+  if (rs_ok && a.tma_store == 1 && !g.epi_stg && !a.bstat) {
+    cuuint64_t dims[3] = {(cuuint64_t)g.N, (cuuint64_t)g.M, (cuuint64_t)rs};
+    cuuint64_t strides[2] = {(cuuint64_t)g.ldd * 4, (cuuint64_t)g.ldd * 4 * g.M};
+    cuuint32_t box[3] = {32, 32, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (g_encode_tiled(&a.tmP, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, g.partial, dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+      const int64_t rem = tiles % 74;
+      a.rs_first = (int)(tiles - rem);
+      a.rs_splits = rs;
+      tiles = a.rs_first + rem * rs;  // work units
+      a.total_tiles = (int)tiles;
+    }
+  }
   if (g.epi_stg && a.tma_store && g.ldd % 4 == 0) a.tma_store = 2;  // tuned variant: LSU-staged stores
   if (a.tma_store != 1) td = tbh;  // unused slot
   if (g.a_mode == A_GATHER) ta = tbh;  // unused operand slot
@@ -1081,7 +1119,22 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   }
   if (e != cudaSuccess) return e;
   if (g.splits > 1) e = launch_split_reduce(g.partial, g.d, (int64_t)g.batch * g.M, g.N, g.ldd, g.splits, s);
+  if (a.rs_splits > 1)
+    e = launch_rsplit_reduce(g.partial, g.d, g.M, g.N, g.ldd, a.rs_first, a.mt * a.nt - a.rs_first, a.nt,
+                             g.block_n, a.rs_splits, s);
   return e;
+}
+
+int gemm2_rsplit_factor(int64_t tiles, int nkb) {
+  // remainder split: only when the tiles fill >= 1 wave of the 74 CTA pairs and the last wave is at most
+  // half full; s splits of the r remainder tiles keep r*s <= 74 and >= 4 k-blocks per split
+  if (tiles < 74) return 0;
+  const int64_t r = tiles % 74;
+  if (r == 0 || r > 37) return 0;
+  int64_t s = 74 / r;
+  if (s > nkb / 4) s = nkb / 4;
+  if (s > 8) s = 8;
+  return s >= 2 ? (int)s : 0;
 }
 
 }  // namespace conv2d

@@ -41,6 +41,8 @@ struct Gemm2Args {
   const float* b_w;        // k = row): MN-major operand, no filter_prep; needs N % 32 == 0, batch 1
   int64_t b_rows;          // (bt_hi / bt_lo unused; 3xTF32 lo halves are split in smem by the kernel)
   bool bstat;              // B-stationary schedule where B-resident applies with several N tiles
+  bool rsplit;             // remainder split of a partial last wave (needs `partial` with
+                           // gemm2_rsplit_factor(tiles, nkb) planes of M x ldd floats)
 };
 
 cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s);
@@ -60,6 +62,10 @@ cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_
 bool gemm2_encode_tiled_sw(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
                            const uint32_t* box, int swizzle);  // swizzle: a CUtensorMapSwizzle value
 int gemm2_choose_block_n(int64_t N);
+// remainder-split factor for `tiles` pair tiles of nkb k-blocks (0 = not applicable)
+int gemm2_rsplit_factor(int64_t tiles, int nkb);
+cudaError_t launch_rsplit_reduce(const float* partial, float* d, int64_t M, int64_t N, int64_t ldd, int first_tile,
+                                 int ntiles, int nt, int block_n, int splits, cudaStream_t s);
 // debug: enable (1) / disable (0) / keep (-1) per-CTA globaltimer stamps of the GEMM kernels (records of
 // 148 CTAs x 8 stamps, one per launch, ring of 256) and optionally copy them to `host` (synchronous);
 // returns values copied.  gemm2_trace_record(): the next launch's record, or null when disabled.

@@ -94,7 +94,50 @@ __global__ void split_reduce_kernel(const float* __restrict__ partial, float* __
   }
 }
 
+// remainder split: d[tile rows, tile cols] = sum_{s} partial[s][...] in fixed order, for the pair tiles
+// [first_tile, first_tile + ntiles) (tile t: M rows [(t / nt)*256, +256), N cols [(t % nt)*BN, +BN)).
+// One thread per float4 of a tile row; ldd % 4 == 0.
+__global__ void rsplit_reduce_kernel(const float* __restrict__ partial, float* __restrict__ d, int64_t M, int64_t N,
+                                     int64_t ldd, int first_tile, int ntiles, int nt, int block_n, int splits) {
+  pdl_trigger();
+  pdl_wait();
+  const int q4 = block_n / 4;
+  const int64_t total = (int64_t)ntiles * 256 * q4;
+  const int64_t plane = M * ldd;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c4 = (int)(i % q4);
+    const int64_t rr = i / q4;
+    const int r = (int)(rr % 256);
+    const int t = first_tile + (int)(rr / 256);
+    const int64_t m = (int64_t)(t / nt) * 256 + r;
+    const int64_t n = (int64_t)(t % nt) * block_n + c4 * 4;
+    if (m >= M || n >= N) continue;
+    const int64_t o = m * ldd + n;
+    float4 acc = *reinterpret_cast<const float4*>(partial + o);
+    for (int s2 = 1; s2 < splits; ++s2) {
+      const float4 v = *reinterpret_cast<const float4*>(partial + s2 * plane + o);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if (n + 3 < N) {
+      *reinterpret_cast<float4*>(d + o) = acc;
+    } else {
+      const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+      for (int e = 0; e < 4 && n + e < N; ++e) d[o + e] = a4[e];
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_rsplit_reduce(const float* partial, float* d, int64_t M, int64_t N, int64_t ldd, int first_tile,
+                                 int ntiles, int nt, int block_n, int splits, cudaStream_t s) {
+  const int64_t total = (int64_t)ntiles * 256 * (block_n / 4);
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  return launch_k(rsplit_reduce_kernel, dim3((unsigned)blocks), dim3(256), 0, s, partial, d, M, N, ldd, first_tile,
+                  ntiles, nt, block_n, splits);
+}
 
 cudaError_t launch_filter_prep2(const float* w, int KH, int KW, int C, int F, int cstride, int rowstride,
                                 int64_t kpad, int64_t npad, float* bt_hi, float* bt_lo, cudaStream_t s) {

@@ -30,6 +30,7 @@ struct Plan {
   bool three_x, pad;
   int block_n, splits, cstride, cg, rowstride, hp, wp;
   bool b_mn;  // B straight from the HWCF filter (no filter_prep launch)
+  bool rsplit;  // remainder split (variant bit 4)
   int64_t kpad, npad;
   size_t bt_bytes, pad_bytes, partial_bytes, total;
 };
@@ -49,7 +50,7 @@ VKey vkey(const Problem& p, bool is_1x1) {
   return VKey(p.N, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH, p.SW, p.pad_top * 64 + p.pad_left, (int)p.math, is_1x1);
 }
 int variant_of(const Problem& p, bool is_1x1) {
-  if (const char* f = getenv("CONV2D_FORCE_VARIANT")) return atoi(f) & 15;  // parity-test hook
+  if (const char* f = getenv("CONV2D_FORCE_VARIANT")) return atoi(f) & 31;  // parity-test hook
   std::lock_guard<std::mutex> lk(g_vmu);
   auto it = g_variant.find(vkey(p, is_1x1));
   return it == g_variant.end() ? 0 : it->second;
@@ -129,6 +130,16 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
                  : rowk ? round_up((int64_t)p.N * pl.hp * pl.wp * pl.cg * 4, 256)
                                          : round_up((int64_t)p.N * p.H * p.W * pl.cg * 4, 256);
   pl.partial_bytes = pl.splits > 1 ? (size_t)pl.splits * p.M() * p.F * 4 : 0;
+  // bit 4: remainder split of a partial last wave (partials for those tiles only, summed by a small kernel)
+  pl.rsplit = false;
+  if ((variant & 16) && pl.splits == 1 && p.F % 4 == 0 && !rowk && pl.a_mode != A_HALO) {
+    const int64_t tiles = ((p.M() + 255) / 256) * ((p.F + pl.block_n - 1) / pl.block_n);
+    const int rs = gemm2_rsplit_factor(tiles, (int)(pl.kpad / 32));
+    if (rs >= 2) {
+      pl.rsplit = true;
+      pl.partial_bytes = (size_t)rs * p.M() * p.F * 4;
+    }
+  }
   pl.total = pl.bt_bytes * (pl.three_x ? 2 : 1) + pl.pad_bytes + pl.partial_bytes;
   return pl;
 }
@@ -142,14 +153,22 @@ int igemm_variants(const Problem& p, bool is_1x1, int* masks) {
   // bit 3 matters only where some A path reads B directly (im2col / dense, F % 32 == 0) in 3xTF32 mode
   const bool alt_b = p.math == CONV2D_MATH_FP32 && p.F % 32 == 0 &&
                      ((is_1x1 && p.C % 4 == 0 && p.C >= 32) || gemm2_im2col_ok(p));
+  // bit 4: remainder split, where the pair-tile count leaves a last wave at most half full
+  auto rs_ok = [&](int m) {
+    const int bn = (m & 2) && gemm2_choose_block_n(p.F) == 256 ? 128 : gemm2_choose_block_n(p.F);
+    const int64_t tiles = ((p.M() + 255) / 256) * ((p.F + bn - 1) / bn);
+    const int64_t K = (int64_t)p.KH * p.KW * p.C;
+    return p.F % 4 == 0 && gemm2_rsplit_factor(tiles, (int)((K + 31) / 32)) >= 2;
+  };
   int n = 0;
   // bit 0: A path, bit 1: N tile, bit 3: B path.  Bit 2 (LSU-staged epilogue) is not enumerated: it
   // measured slower than TMA stores on every paper layer (reachable through CONV2D_FORCE_VARIANT).
-  for (int m = 0; m < 16; ++m) {
+  for (int m = 0; m < 32; ++m) {
     if (m & 4) continue;
     if ((m & 1) && !alt_a) continue;
     if ((m & 2) && !alt_n) continue;
     if ((m & 8) && !alt_b) continue;
+    if ((m & 16) && !rs_ok(m)) continue;
     if (masks) masks[n] = m;
     ++n;
   }
@@ -171,7 +190,7 @@ void igemm_set_variant(const Problem& p, bool is_1x1, int v) {
 
 size_t igemm_workspace(const Problem& p, bool is_1x1) {
   size_t w = 0;
-  int masks[16];
+  int masks[32];
   const int n = igemm_variants(p, is_1x1, masks);
   for (int i = 0; i < n; ++i) w = std::max(w, make_plan(p, is_1x1, masks[i]).total);
   return w;
@@ -180,7 +199,7 @@ size_t igemm_workspace(const Problem& p, bool is_1x1) {
 int igemm_launches(const Problem& p, bool is_1x1) {
   const Plan pl = make_plan(p, is_1x1, variant_of(p, is_1x1));
   if (pl.a_mode == A_S2D) return (p.C <= 3 && ((int64_t)p.W * p.C) % 4 == 0) ? 2 : 3;  // [s2d input,] filter, GEMM
-  return (pl.b_mn ? 1 : 2) + (pl.pad ? 1 : 0) + (pl.splits > 1 ? 1 : 0);
+  return (pl.b_mn ? 1 : 2) + (pl.pad ? 1 : 0) + (pl.splits > 1 || pl.rsplit ? 1 : 0);
 }
 
 cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const float* filt, float* out, void* ws,
@@ -211,7 +230,7 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
     if (e != cudaSuccess) return e;
     xg = xp;
   }
-  float* partial = pl.splits > 1 ? reinterpret_cast<float*>(w8) : nullptr;
+  float* partial = (pl.splits > 1 || pl.rsplit) ? reinterpret_cast<float*>(w8) : nullptr;
   if (!pl.b_mn) {
     cudaError_t e =
         launch_filter_prep2(filt, p.KH, p.KW, p.C, p.F, pl.cstride, pl.rowstride, pl.kpad, pl.npad, bt_hi, bt_lo, s);
@@ -243,6 +262,7 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
   g.wp = pl.wp;
   g.epi_stg = (variant_of(p, is_1x1) & 4) != 0;
   g.b_mn = pl.b_mn;
+  g.rsplit = pl.rsplit;
   g.b_w = filt;
   g.b_rows = (int64_t)p.KH * p.KW * p.C;
   return launch_gemm2(p, g, s);

@@ -20,6 +20,8 @@
 // workspace (the GEMMs run on the tensor cores); the fused form is DESIGN.md "Next".
 // TF32 mode rounds U and V to TF32 with cvt.rna (reading R16); FP32 mode runs the GEMMs
 // in 3xTF32.
+#include <cstdlib>
+
 #include "gemm2sm.h"
 #include "launch.cuh"
 #include "sm100.cuh"

@@ -231,10 +231,13 @@ def test_tf32_mma_reads_truncated_operands(cuda_ok):
     assert np.array_equal(gpu_conv(p, x, w, a), gpu_conv(p, xt, wt, a))
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 7, 8, 11])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 7, 8, 11, 16, 17, 18, 24])
 @pytest.mark.parametrize("case", [(2, 28, 28, 64, 64, 3, 3, 1, 1, 0), (1, 14, 15, 128, 128, 3, 3, 1, 1, 1),
                                   (2, 12, 12, 64, 256, 1, 1, 1, 1, 0), (1, 9, 9, 64, 320, 3, 3, 2, 2, 0),
-                                  (2, 21, 19, 3, 36, 7, 7, 2, 2, 0)], ids=str)
+                                  (2, 21, 19, 3, 36, 7, 7, 2, 2, 0),
+                                  # remainder split: 150 / 85 / 100 pair tiles (last wave 2 / 11 / 26 of 74)
+                                  (2, 150, 128, 256, 64, 1, 1, 1, 1, 0), (5, 68, 64, 96, 128, 3, 3, 1, 1, 0),
+                                  (8, 28, 28, 256, 1024, 1, 1, 1, 1, 0)], ids=str)
 def test_algorithm_parameter_variants(cuda_ok, monkeypatch, variant, case):
     """Both A-operand variants the auto-selector may pick per layer (implicit_gemm: halo <-> im2col,
     matmul_1x1: dense <-> im2col) give the same results (integer-exact and within tolerance)."""
