@@ -673,10 +673,6 @@ cudaError_t launch_gemm_s2d(const Problem& p, const float* in, const float* filt
     }
     if (any) st.code[st.n++] = (uint8_t)code;
   }
-  if (getenv("CONV2D_EXPERIMENT_ALL_STEPS")) {  // A/B: issue every step in natural order
-    st.n = 32;
-    for (int c = 0; c < 32; ++c) st.code[c] = (uint8_t)c;
-  }
   for (int c = st.n; c < 32; ++c) st.code[c] = st.code[0];  // padding steps: any view, zero B rows
   // raw mode (C <= 3, 16-byte input rows): the GEMM builds s2d halos from raw input patches itself
   const bool raw = p.C <= 3 && ((int64_t)p.W * p.C) % 4 == 0 && getenv("CONV2D_S2D_PREPASS") == nullptr;
