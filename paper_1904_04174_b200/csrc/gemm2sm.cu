@@ -545,6 +545,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           cp_async_commit();
           if (it >= (uint32_t)LAG) {
             cp_async_wait<LAG>();
+            // finalize reads whole A rows (LO_TMEM: thread t <- row t), gathered by other threads' cp.asyncs:
+            // every transform thread's groups for that stage must have landed (named barrier, warps 0-3)
+            named_bar_sync(1, 128);
             finalize(it - LAG);
           }
         }
@@ -598,6 +601,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     }
     if (AMODE == A_GATHER) {
       cp_async_wait<0>();
+      named_bar_sync(1, 128);  // all transform threads' gathers landed (see above)
       for (uint32_t jt = (it > (uint32_t)LAG ? it - LAG : 0); jt < it; ++jt) finalize(jt);
     }
     if (THREE_X && !C_::LO_TMEM) {  // drain: every lo slot released before exit (multicast commits target us)

@@ -128,6 +128,10 @@ EDGE = [
     (2, 10, 10, 48, 64, 1, 1, 1, 1, 0),
     (1, 6, 40, 64, 288, 1, 1, 1, 1, 0),
     (1, 15, 13, 128, 160, 3, 3, 2, 2, 0),
+    # gather A path (C % 32 != 0) + 3xTF32 lo halves in TMEM (BN <= 128): each thread's lo row is gathered by
+    # other threads' cp.asyncs (regression: tools/fuzz_gpu.py found the missing barrier)
+    (1, 44, 43, 48, 100, 1, 1, 1, 1, 0),
+    (3, 21, 26, 40, 64, 3, 3, 2, 2, 1),
     # space-to-depth stem path (K in {7, 8}, stride 2, C <= 4, F <= 128): ragged 8x16 output tiles,
     # odd image sizes, SAME corners, VALID, C = 1 / 2 / 4, K = 8, F not a multiple of 32
     (1, 37, 29, 3, 64, 7, 7, 2, 2, 0),

@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Run one conv2d_forward through the C-ABI and compare with the oracle (debug helper).
     python tools/probe_conv.py N H W C F KH KW SH SW PAD [math] [algo]"""
+import os
 import sys
 import numpy as np
 import torch
@@ -13,8 +14,13 @@ math = int(sys.argv[11]) if len(sys.argv) > 11 else 0
 algo = C.ALGO_BY_NAME[sys.argv[12]] if len(sys.argv) > 12 else C.ALGO_IMPLICIT_GEMM
 n, h, w, c, f, kh, kw, sh, sw, pad = a
 rng = np.random.default_rng(1)
-x = rng.integers(-2, 3, size=(n, h, w, c)).astype(np.float32)
-wt = rng.integers(-2, 3, size=(kh, kw, c, f)).astype(np.float32)
+uniform = os.environ.get("PROBE_UNIFORM") is not None
+if uniform:
+    x = rng.uniform(-1, 1, size=(n, h, w, c)).astype(np.float32)
+    wt = rng.uniform(-1, 1, size=(kh, kw, c, f)).astype(np.float32)
+else:
+    x = rng.integers(-2, 3, size=(n, h, w, c)).astype(np.float32)
+    wt = rng.integers(-2, 3, size=(kh, kw, c, f)).astype(np.float32)
 p = C.Params(n, h, w, c, f, kh, kw, sh, sw, pad, math=math)
 (N, ho, wo, F), _ = C.conv2d_output_shape(p)
 y = torch.full((N * ho * wo * F,), float("nan"), device="cuda")
@@ -22,7 +28,12 @@ ws = torch.empty(max(C.conv2d_query_workspace(p, algo), 16), dtype=torch.uint8, 
 C.conv2d_forward(p, algo, torch.from_numpy(x).cuda(), torch.from_numpy(wt).cuda(), y, ws, ws.numel())
 torch.cuda.synchronize()
 O.build()
-ref = O.conv2d(O.Params(n, h, w, c, f, kh, kw, sh, sw, pad), x.astype(np.float64), wt.astype(np.float64))
+ref, den = O.conv2d(O.Params(n, h, w, c, f, kh, kw, sh, sw, pad), x, wt, with_denom=True)
 got = y.cpu().numpy().reshape(ref.shape)
-bad = np.argwhere(got != ref)
-print(a, "bad", len(bad), "of", got.size, bad[:4].tolist())
+if uniform:
+    e = np.abs(got.astype(np.float64) - ref) / den
+    bad = np.argwhere(e > 1e-5)
+    print(a, "norm err %.3e" % e.max(), "bad", len(bad), bad[:6].tolist())
+else:
+    bad = np.argwhere(got != ref)
+    print(a, "bad", len(bad), "of", got.size, bad[:4].tolist())
