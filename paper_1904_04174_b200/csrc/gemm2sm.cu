@@ -68,6 +68,7 @@ struct DevArgs {
   alignas(64) CUtensorMap tmP;  // partial planes {N, M, s} (remainder split only)
   int bstat;  // B-stationary schedule (B-resident with several N tiles): pair p owns N tile p % nt
   int b_mn;  // 1: B read straight from the row-major K x F filter (MN-major operand; no filter_prep)
+  int early;  // 1: 3xTF32 relay A paths issue the first stages before the cluster barrier completes
   unsigned long long* trace;  // debug (conv2d_debug_trace): TRACE_SLOTS globaltimer stamps per CTA, or null
 };
 
@@ -191,7 +192,95 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   if (threadIdx.x == 0) trace_at(args, 0);
   pdl_trigger();  // launch.cuh: the next kernel may start its prologue while this one runs
 
-  if (threadIdx.x == 0) {
+  const uint32_t full_leader = mapa(smem_u32(full), 0);
+  // A_NARROW: k-block kb = 8 (tap, channel-quad) boxes of 128 px x 16 B, box q at +2 KB;
+  // taps past Kh*Kw get an out-of-image offset so the TMA zero-fills them.
+  const int nq = args.Cg / 4;
+  const int taps = args.KH * args.KW;
+  auto narrow_box = [&](int kb, int q, int& c, uint16_t& ow, uint16_t& oh) {
+    const int idx = kb * 8 + q;
+    const int tap = idx / nq;
+    c = (idx - tap * nq) * 4;
+    if (tap < taps) {
+      ow = (uint16_t)(tap % args.KW);
+      oh = (uint16_t)(tap / args.KW);
+    } else {
+      ow = 0xFFFF;
+      oh = 0xFFFF;
+      c = 0;
+    }
+  };
+  auto narrow_loads = [&](uint64_t* bar, uint32_t dst, int kb, int wb, int hb, int nimg) {
+#pragma unroll 1
+    for (int q = 0; q < 8; ++q) {
+      int c;
+      uint16_t ow, oh;
+      narrow_box(kb, q, c, ow, oh);
+      tma_load_im2col_4d(&tmA, bar, dst + q * 2048, c, wb, hb, nimg, ow, oh);
+    }
+  };
+  auto narrow_loads_2sm = [&](uint32_t bar, uint32_t dst, int kb, int wb, int hb, int nimg) {
+#pragma unroll 1
+    for (int q = 0; q < 8; ++q) {
+      int c;
+      uint16_t ow, oh;
+      narrow_box(kb, q, c, ow, oh);
+      tma_load_im2col_4d_2sm(&tmA, bar, dst + q * 2048, c, wb, hb, nimg, ow, oh);
+    }
+  };
+  // b_mn: B box = {32 n, 32 k, BN/64 n-chunks} of the 3-D view {n % 32, k, n / 32} of the HWCF
+  // filter; only hi (= the raw fp32) comes by TMA, the transform warps derive lo in smem.
+  const bool bmn = args.b_mn != 0;
+  const int b_copies = (THREE_X && !bmn) ? 2 : 1;
+  // A_ROWSEG boxes are exactly KW*C4 floats wide (no OOB elements -> TMA fast path): fewer bytes
+  const uint32_t a_bytes = AMODE == A_GATHER ? 0u : AMODE == A_ROWSEG ? (uint32_t)args.a_row_bytes * 128u : A_TILE;
+  const uint32_t bytes = a_bytes + (BRES ? 0u : (uint32_t)(b_copies * C_::BHALF));
+  // tile -> TMA coordinates of this CTA's A rows (m_cta / image window) and B half (nrow)
+  auto coords = [&](const Tile& tl, int64_t& m_cta, int& wb, int& hb, int& nimg, int& nrow) {
+    m_cta = (int64_t)tl.mi * 2 * BMC + rank * BMC;
+    wb = hb = nimg = 0;
+    if (SPATIAL) {
+      wb = (tl.mi % args.wblk) * 16;
+      hb = ((tl.mi / args.wblk) % args.hblk) * 16 + (int)rank * 8;
+      nimg = tl.mi / (args.wblk * args.hblk);
+    } else if (AMODE == A_IM2COL || AMODE == A_NARROW) {
+      const int64_t hw = (int64_t)args.HO * args.WO;
+      nimg = (int)(m_cta / hw);
+      const int rem = (int)(m_cta % hw);
+      wb = (rem % args.WO) * args.SW - args.PL;
+      hb = (rem / args.WO) * args.SH - args.PT;
+    }
+    nrow = tl.ni * BN + (int)rank * (BN / 2);
+  };
+  // RELAY stage s <- k-block kb: A (and the per-stage B) into this CTA's smem, on its own ld_full[s]
+  auto relay_load = [&](int s, int kb, const Tile& tl, int64_t m_cta, int wb, int hb, int nimg, int nrow) {
+    const int tap = AMODE == A_IM2COL ? kb / args.ncb : 0;
+    const int cb = AMODE == A_IM2COL ? kb - tap * args.ncb : 0;
+    mbar_arrive_expect_tx(&ld_full[s], bytes);
+    if (AMODE == A_IM2COL)
+      tma_load_im2col_4d(&tmA, &ld_full[s], smem_u32(a_hi(s)), cb * BK, wb, hb, nimg, (uint16_t)(tap % args.KW),
+                         (uint16_t)(tap / args.KW));
+    else if (AMODE == A_NARROW)
+      narrow_loads(&ld_full[s], smem_u32(a_hi(s)), kb, wb, hb, nimg);
+    else if (AMODE == A_ROWSEG)
+      tma_load_5d(&tmA, &ld_full[s], smem_u32(a_hi(s)), 0, wb, hb, nimg, kb);
+    else if (AMODE == A_DENSE)
+      tma_load_3d(&tmA, &ld_full[s], smem_u32(a_hi(s)), kb * BK, (int)m_cta, tl.bz);
+    if (!BRES && bmn) {
+      tma_load_3d(&tmBh, &ld_full[s], smem_u32(b_hi(s)), 0, kb * BK, nrow / 32);
+    } else if (!BRES) {
+      tma_load_3d(&tmBh, &ld_full[s], smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
+      if (THREE_X) tma_load_3d(&tmBl, &ld_full[s], smem_u32(b_lo(s)), kb * BK, nrow, tl.bz);
+    }
+  };
+  // 3xTF32 relay loads signal only this CTA's own ld_full barriers, so the producer thread initialises
+  // the barriers itself and issues the first tile's first S k-blocks after its cluster-barrier arrival,
+  // before the barrier completes: the first loads' latency hides behind the CTA-pair setup (excluded:
+  // A paths whose stages are zero-filled first, the gather and the stem halo)
+  const bool early = THREE_X && args.early && (AMODE == A_IM2COL || AMODE == A_DENSE || AMODE == A_NARROW ||
+                                 (AMODE == A_ROWSEG && args.a_row_bytes == 128));
+  uint32_t pre = 0;  // producer: k-block iterations already issued
+  if (warp == 4 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&ld_full[s], 1);
       // RELAY: both CTAs' 128 transform threads (+ 128 B-split threads each when they run) arrive
@@ -210,8 +299,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       mbar_init(&hs_empty[h], 128);
     }
     fence_mbar_init();
-  }
-  if (warp == 4 && lane == 0) {
     if (AMODE != A_GATHER) tma_prefetch(&tmA);
     tma_prefetch(&tmBh);
     if (THREE_X) tma_prefetch(&tmBl);
@@ -225,7 +312,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   }
   if (warp == 5) tmem_alloc_2sm<C_::TMEM_COLS>(tmem_slot);
   tc_fence_before();
-  cluster_sync();
+  cluster_arrive();
+  // between this CTA's arrival and the cluster barrier's completion (no thread waits on the producer)
+  if (early && warp == 4 && lane == 0) {
+    const int t0 = tile_at(args, cid, ncl, 0);
+    if (t0 >= 0) {
+      pdl_wait();
+      const Tile tl = decode(args, t0);
+      int64_t m_cta;
+      int wb, hb, nimg, nrow;
+      coords(tl, m_cta, wb, hb, nimg, nrow);
+      trace_at(args, 2);
+      for (int kb = tl.kb0; kb < tl.kb1 && pre < (uint32_t)S; ++kb, ++pre)
+        relay_load((int)pre, kb, tl, m_cta, wb, hb, nimg, nrow);
+    }
+  }
+  __syncwarp();
+  cluster_wait();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();  // first global-memory access below: the previous kernel has completed
@@ -234,50 +337,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   if (warp == 4) {
     // ============================ TMA producer ============================
     if (lane == 0) {
-      const uint32_t full_leader = mapa(smem_u32(full), 0);
-      // A_NARROW: k-block kb = 8 (tap, channel-quad) boxes of 128 px x 16 B, box q at +2 KB;
-      // taps past Kh*Kw get an out-of-image offset so the TMA zero-fills them.
-      const int nq = args.Cg / 4;
-      const int taps = args.KH * args.KW;
-      auto narrow_box = [&](int kb, int q, int& c, uint16_t& ow, uint16_t& oh) {
-        const int idx = kb * 8 + q;
-        const int tap = idx / nq;
-        c = (idx - tap * nq) * 4;
-        if (tap < taps) {
-          ow = (uint16_t)(tap % args.KW);
-          oh = (uint16_t)(tap / args.KW);
-        } else {
-          ow = 0xFFFF;
-          oh = 0xFFFF;
-          c = 0;
-        }
-      };
-      auto narrow_loads = [&](uint64_t* bar, uint32_t dst, int kb, int wb, int hb, int nimg) {
-#pragma unroll 1
-        for (int q = 0; q < 8; ++q) {
-          int c;
-          uint16_t ow, oh;
-          narrow_box(kb, q, c, ow, oh);
-          tma_load_im2col_4d(&tmA, bar, dst + q * 2048, c, wb, hb, nimg, ow, oh);
-        }
-      };
-      auto narrow_loads_2sm = [&](uint32_t bar, uint32_t dst, int kb, int wb, int hb, int nimg) {
-#pragma unroll 1
-        for (int q = 0; q < 8; ++q) {
-          int c;
-          uint16_t ow, oh;
-          narrow_box(kb, q, c, ow, oh);
-          tma_load_im2col_4d_2sm(&tmA, bar, dst + q * 2048, c, wb, hb, nimg, ow, oh);
-        }
-      };
       uint32_t it = 0;
-      // b_mn: B box = {32 n, 32 k, BN/64 n-chunks} of the 3-D view {n % 32, k, n / 32} of the HWCF
-      // filter; only hi (= the raw fp32) comes by TMA, the transform warps derive lo in smem.
-      const bool bmn = args.b_mn != 0;
-      const int b_copies = (THREE_X && !bmn) ? 2 : 1;
-      // A_ROWSEG boxes are exactly KW*C4 floats wide (no OOB elements -> TMA fast path): fewer bytes
-      const uint32_t a_bytes = AMODE == A_GATHER ? 0u : AMODE == A_ROWSEG ? (uint32_t)args.a_row_bytes * 128u : A_TILE;
-      const uint32_t bytes = a_bytes + (BRES ? 0u : (uint32_t)(b_copies * C_::BHALF));
       // BRES: this CTA's B half of the pair's N tile (tile ni: rows [ni*BN + rank*BN/2, +BN/2)), once
       const int res_row = (args.bstat ? (cid % args.nt) * BN : 0) + (int)rank * (BN / 2);
       if (BRES && bmn && THREE_X) {  // own B half into own smem; the transform warps split it, then signal
@@ -311,21 +371,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       }
       for (int t, jj = 0; AMODE != A_STEM && (t = tile_at(args, cid, ncl, jj)) >= 0; ++jj) {
         const Tile tl = decode(args, t);
-        const int64_t m_cta = (int64_t)tl.mi * 2 * BMC + rank * BMC;
-        int wb = 0, hb = 0, nimg = 0;
-        if (SPATIAL) {
-          wb = (tl.mi % args.wblk) * 16;
-          hb = ((tl.mi / args.wblk) % args.hblk) * 16 + (int)rank * 8;
-          nimg = tl.mi / (args.wblk * args.hblk);
-        } else if (AMODE == A_IM2COL || AMODE == A_NARROW) {
-          const int64_t hw = (int64_t)args.HO * args.WO;
-          nimg = (int)(m_cta / hw);
-          const int rem = (int)(m_cta % hw);
-          wb = (rem % args.WO) * args.SW - args.PL;
-          hb = (rem / args.WO) * args.SH - args.PT;
-        }
-        const int nrow = tl.ni * BN + (int)rank * (BN / 2);
+        int64_t m_cta;
+        int wb, hb, nimg, nrow;
+        coords(tl, m_cta, wb, hb, nimg, nrow);
         for (int kb = tl.kb0; kb < tl.kb1; ++kb, ++it) {
+          if (it < pre) continue;  // issued before the cluster barrier
           const int s = it % S;
           const uint32_t u = it / S;
           if (u > 0) mbar_wait(&empty[s], (u - 1) & 1);
@@ -333,22 +383,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const int tap = AMODE == A_IM2COL ? kb / args.ncb : 0;
           const int cb = AMODE == A_IM2COL ? kb - tap * args.ncb : 0;
           if (RELAY) {
-            mbar_arrive_expect_tx(&ld_full[s], bytes);
-            if (AMODE == A_IM2COL)
-              tma_load_im2col_4d(&tmA, &ld_full[s], smem_u32(a_hi(s)), cb * BK, wb, hb, nimg,
-                                 (uint16_t)(tap % args.KW), (uint16_t)(tap / args.KW));
-            else if (AMODE == A_NARROW)
-              narrow_loads(&ld_full[s], smem_u32(a_hi(s)), kb, wb, hb, nimg);
-            else if (AMODE == A_ROWSEG)
-              tma_load_5d(&tmA, &ld_full[s], smem_u32(a_hi(s)), 0, wb, hb, nimg, kb);
-            else if (AMODE == A_DENSE)
-              tma_load_3d(&tmA, &ld_full[s], smem_u32(a_hi(s)), kb * BK, (int)m_cta, tl.bz);
-            if (!BRES && bmn) {
-              tma_load_3d(&tmBh, &ld_full[s], smem_u32(b_hi(s)), 0, kb * BK, nrow / 32);
-            } else if (!BRES) {
-              tma_load_3d(&tmBh, &ld_full[s], smem_u32(b_hi(s)), kb * BK, nrow, tl.bz);
-              if (THREE_X) tma_load_3d(&tmBl, &ld_full[s], smem_u32(b_lo(s)), kb * BK, nrow, tl.bz);
-            }
+            relay_load(s, kb, tl, m_cta, wb, hb, nimg, nrow);
           } else {
             // both CTAs' bytes land on the leader's full[s]; only the leader arms it
             if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes);
@@ -1021,6 +1056,8 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   a.d = g.d; a.ldd = g.ldd; a.d_bstride = g.d_batch_stride; a.partial = g.partial;
   a.trace = gemm2_trace_record();
   a.b_mn = g.b_mn ? 1 : 0;
+  static const bool no_early = getenv("CONV2D_NO_EARLY_TMA") != nullptr;  // A/B switch (DESIGN.md env hooks)
+  a.early = no_early ? 0 : 1;
   {  // B-stationary: several N tiles, each owned by >= 1 pair, B half resident (short K)
     const int kbmax = g.block_n == 64 ? (g.three_x ? Cfg<64, true, true>::RES_KB_MAX : Cfg<64, false, true>::RES_KB_MAX)
                       : g.block_n == 128 ? (g.three_x ? Cfg<128, true, true>::RES_KB_MAX : Cfg<128, false, true>::RES_KB_MAX)
