@@ -422,11 +422,13 @@ def main():
     g_bytes = sum(cv["bytes"] for cv, _ in grp)
     ach = g_flops / (g_ms / 1e3) / 1e12
     traffic, traffic_src = None, None
-    tpath = os.path.join(ROOT, "profiles", "round1_step_traffic.json")
+    # ncu traffic of the same workload only (tools/step_traffic.py records the batch it was captured at)
+    tname = "round1_step_traffic.json" if args.global_batch == 256 else f"round1_step_traffic_b{args.global_batch}.json"
+    tpath = os.path.join(ROOT, "profiles", tname)
     if os.path.exists(tpath) and world == 1 and math == C.MATH_FP32:
         with open(tpath) as fh:
             tj = json.load(fh)
-        if tj.get("gemm_launches"):
+        if tj.get("gemm_launches") and tj.get("global_batch", 256) == args.global_batch:
             traffic = round(tj["gemm_dram_bytes"] / tj["gemm_launches"] / 1e6, 2)
             traffic_src = (f"MB per GEMM-core launch (gemm2sm / halo), ncu dram__bytes_read.sum+write.sum over one "
                            f"timed step ({tj['gemm_launches']} launches; profiles/round1_ncu.md)")

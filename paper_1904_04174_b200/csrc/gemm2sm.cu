@@ -1166,16 +1166,34 @@ cudaError_t launch_gemm2(const Problem& p, const Gemm2Args& g, cudaStream_t s) {
   return e;
 }
 
+// Modelled time, in k-block units, of `tiles` pair tiles of nkb k-blocks on the 74 CTA pairs when the
+// last r tiles are cut into s K ranges (r == tiles: every tile): each wave of units costs its k-blocks
+// plus a pipeline fill/drain of ~2 k-blocks; any split adds the partial planes' write + reduce (~4).
+static int64_t split_cost(int64_t tiles, int64_t r, int s, int nkb) {
+  const int64_t waves_whole = (tiles - r) / 74;
+  const int64_t waves_split = (r * s + 73) / 74;
+  return waves_whole * (nkb + 2) + waves_split * ((nkb + s - 1) / s + 2) + (s > 1 ? 4 : 0);
+}
+
+int gemm2_balanced_splits(int64_t tiles, int nkb) {
+  // fewer pair tiles than pairs: the K-split count (<= 16, >= 4 k-blocks each) of least modelled time
+  if (tiles <= 0 || tiles >= 74) return 1;
+  int best = 1;
+  for (int s = 2; s <= 16 && s <= nkb / 4; ++s)
+    if (split_cost(tiles, tiles, s, nkb) < split_cost(tiles, tiles, best, nkb)) best = s;
+  return best;
+}
+
 int gemm2_rsplit_factor(int64_t tiles, int nkb) {
-  // remainder split: only when the tiles fill >= 1 wave of the 74 CTA pairs and the last wave is at most
-  // half full; s splits of the r remainder tiles keep r*s <= 74 and >= 4 k-blocks per split
+  // remainder split: the tiles fill >= 1 wave of the 74 CTA pairs; the r = tiles % 74 tiles of the
+  // partial last wave are cut into s <= 8 K ranges (>= 4 k-blocks each) of least modelled time
   if (tiles < 74) return 0;
   const int64_t r = tiles % 74;
-  if (r == 0 || r > 37) return 0;
-  int64_t s = 74 / r;
-  if (s > nkb / 4) s = nkb / 4;
-  if (s > 8) s = 8;
-  return s >= 2 ? (int)s : 0;
+  if (r == 0) return 0;
+  int best = 1;
+  for (int s = 2; s <= 8 && s <= nkb / 4; ++s)
+    if (split_cost(tiles, r, s, nkb) < split_cost(tiles, r, best, nkb)) best = s;
+  return best >= 2 ? best : 0;
 }
 
 }  // namespace conv2d

@@ -64,6 +64,8 @@ bool gemm2_encode_tiled_sw(CUtensorMap* m, int rank, const void* base, const uin
 int gemm2_choose_block_n(int64_t N);
 // remainder-split factor for `tiles` pair tiles of nkb k-blocks (0 = not applicable)
 int gemm2_rsplit_factor(int64_t tiles, int nkb);
+// K-split count of least modelled time for fewer than 74 pair tiles (1 = no split)
+int gemm2_balanced_splits(int64_t tiles, int nkb);
 cudaError_t launch_rsplit_reduce(const float* partial, float* d, int64_t M, int64_t N, int64_t ldd, int first_tile,
                                  int ntiles, int nt, int block_n, int splits, cudaStream_t s);
 // debug: enable (1) / disable (0) / keep (-1) per-CTA globaltimer stamps of the GEMM kernels (records of

@@ -130,10 +130,15 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
                  : rowk ? round_up((int64_t)p.N * pl.hp * pl.wp * pl.cg * 4, 256)
                                          : round_up((int64_t)p.N * p.H * p.W * pl.cg * 4, 256);
   pl.partial_bytes = pl.splits > 1 ? (size_t)pl.splits * p.M() * p.F * 4 : 0;
-  // bit 4: remainder split of a partial last wave (partials for those tiles only, summed by a small kernel)
+  // bit 4: balanced K split -- fewer pair tiles than pairs: the modelled-best split count instead of
+  // 74 / tiles; else a remainder split of the partial last wave (partials for those tiles only, summed
+  // by a small kernel)
   pl.rsplit = false;
-  if ((variant & 16) && pl.splits == 1 && p.F % 4 == 0 && !rowk && pl.a_mode != A_HALO) {
-    const int64_t tiles = ((p.M() + 255) / 256) * ((p.F + pl.block_n - 1) / pl.block_n);
+  const int64_t tiles = ((p.M() + 255) / 256) * ((p.F + pl.block_n - 1) / pl.block_n);
+  if ((variant & 16) && tiles < 74 && p.F % 4 == 0 && !rowk && pl.a_mode != A_HALO) {
+    pl.splits = gemm2_balanced_splits(tiles, (int)(pl.kpad / 32));
+    pl.partial_bytes = pl.splits > 1 ? (size_t)pl.splits * p.M() * p.F * 4 : 0;
+  } else if ((variant & 16) && pl.splits == 1 && p.F % 4 == 0 && !rowk && pl.a_mode != A_HALO) {
     const int rs = gemm2_rsplit_factor(tiles, (int)(pl.kpad / 32));
     if (rs >= 2) {
       pl.rsplit = true;
@@ -153,12 +158,15 @@ int igemm_variants(const Problem& p, bool is_1x1, int* masks) {
   // bit 3 matters only where some A path reads B directly (im2col / dense, F % 32 == 0) in 3xTF32 mode
   const bool alt_b = p.math == CONV2D_MATH_FP32 && p.F % 32 == 0 &&
                      ((is_1x1 && p.C % 4 == 0 && p.C >= 32) || gemm2_im2col_ok(p));
-  // bit 4: remainder split, where the pair-tile count leaves a last wave at most half full
+  // bit 4: balanced K split (fewer pair tiles than pairs, where it differs from the default 74 / tiles)
+  // or remainder split (a partial last wave)
   auto rs_ok = [&](int m) {
     const int bn = (m & 2) && gemm2_choose_block_n(p.F) == 256 ? 128 : gemm2_choose_block_n(p.F);
     const int64_t tiles = ((p.M() + 255) / 256) * ((p.F + bn - 1) / bn);
-    const int64_t K = (int64_t)p.KH * p.KW * p.C;
-    return p.F % 4 == 0 && gemm2_rsplit_factor(tiles, (int)((K + 31) / 32)) >= 2;
+    const int nkb = (int)(((int64_t)p.KH * p.KW * p.C + 31) / 32);
+    if (p.F % 4 != 0) return false;
+    if (tiles < 74) return gemm2_balanced_splits(tiles, nkb) != gemm2_choose_splits(p.M(), p.F, nkb, 1, bn);
+    return gemm2_rsplit_factor(tiles, nkb) >= 2;
   };
   int n = 0;
   // bit 0: A path, bit 1: N tile, bit 3: B path.  Bit 2 (LSU-staged epilogue) is not enumerated: it

@@ -241,7 +241,9 @@ def test_tf32_mma_reads_truncated_operands(cuda_ok):
                                   (2, 21, 19, 3, 36, 7, 7, 2, 2, 0),
                                   # remainder split: 150 / 85 / 100 pair tiles (last wave 2 / 11 / 26 of 74)
                                   (2, 150, 128, 256, 64, 1, 1, 1, 1, 0), (5, 68, 64, 96, 128, 3, 3, 1, 1, 0),
-                                  (8, 28, 28, 256, 1024, 1, 1, 1, 1, 0)], ids=str)
+                                  (8, 28, 28, 256, 1024, 1, 1, 1, 1, 0),
+                                  # balanced K split: 40 pair tiles of 32 k-blocks (74 / 40 = 1 -> modelled best 3)
+                                  (10, 32, 32, 1024, 64, 1, 1, 1, 1, 0)], ids=str)
 def test_algorithm_parameter_variants(cuda_ok, monkeypatch, variant, case):
     """Both A-operand variants the auto-selector may pick per layer (implicit_gemm: halo <-> im2col,
     matmul_1x1: dense <-> im2col) give the same results (integer-exact and within tolerance)."""

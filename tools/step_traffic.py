@@ -3,7 +3,10 @@
 taken with --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum over the
 NVTX range "bench_timed" (one step).  Writes the JSON bench.py's roofline.traffic reads.
 
-    python tools/step_traffic.py gpurun_out/launches.csv > profiles/round1_step_traffic.json
+    python tools/step_traffic.py gpurun_out/launches.csv [global_batch=256] > profiles/round1_step_traffic.json
+
+(bench.py uses the file only for the workload it was captured on: b256 -> round1_step_traffic.json,
+any other batch B -> round1_step_traffic_b{B}.json.)
 """
 import csv
 import json
@@ -16,6 +19,7 @@ GEMM = re.compile(r"gemm2sm_kernel|halo_kernel")
 
 def main():
     path = sys.argv[1]
+    batch = int(sys.argv[2]) if len(sys.argv) > 2 else 256
     with open(path) as f:
         lines = [l for l in f if l.startswith('"')]
     per = defaultdict(dict)
@@ -32,7 +36,7 @@ def main():
             n += 1
             us += t
             byts += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
-    json.dump({"source": path, "gemm_launches": n, "gemm_us": us, "gemm_dram_bytes": byts, "total_us": total},
+    json.dump({"source": path, "global_batch": batch, "gemm_launches": n, "gemm_us": us, "gemm_dram_bytes": byts, "total_us": total},
               sys.stdout, indent=1)
     print()
 
