@@ -295,8 +295,8 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
-    # ---- auto-selection (measured, once per distinct layer); rank 0's choices broadcast so every
-    #      rank runs the same kernels (off the timed path)
+    # ---- auto-selection (measured, once per distinct layer); rank 0's choices (algorithm + tuned
+    #      variant) broadcast so every rank runs the same kernels (off the timed path)
     chosen = {}
     C.conv2d_set_autotune_flush(flush)  # cache-cold candidate timings, as in the timed step
     if args.load_selection:
@@ -310,10 +310,16 @@ def main():
     if args.save_selection and rank == 0:
         C.conv2d_save_selection(args.save_selection)
     C.conv2d_set_autotune_flush(None)
-    chosen = broadcast_choices(chosen, dist if world > 1 else None, dev)
+    gemm_like = (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1)
+    chosen = {k: (a, C.conv2d_get_variant(next(cv["p"] for cv in convs if cv["layer"].name == k), a)
+                  if a in gemm_like else 0) for k, a in chosen.items()}
+    chosen = broadcast_choices(chosen, dist if world > 1 else None, dev)  # (algorithm, variant) pairs
     for cv in convs:
-        C.conv2d_set_selected(cv["p"], chosen[cv["layer"].name])
-        cv["algo"] = chosen[cv["layer"].name]
+        a, v = chosen[cv["layer"].name]
+        C.conv2d_set_selected(cv["p"], a)
+        if a in gemm_like:
+            C.conv2d_set_variant(cv["p"], a, v)
+        cv["algo"] = a
         cv["launches"] = C.conv2d_launch_count(cv["p"], C.ALGO_AUTO)
 
     def step(evs=None):

@@ -128,6 +128,16 @@ conv2d_status_t conv2d_selected(const conv2d_params_t* p, conv2d_algo_t* chosen)
  * Fails with CONV2D_ERR_UNSUPPORTED if `algo` cannot run `p`. */
 conv2d_status_t conv2d_set_selected(const conv2d_params_t* p, conv2d_algo_t algo);
 
+/* Tuned parameter variant of the implicit_gemm / matmul_1x1 kernels for `p` (the "/variant" of the
+ * selection table below; a bit mask: A-operand path, N tile, B path, K split -- igemm.cu).
+ * get: *variant = the variant conv2d_autotune / load_selection / set_variant recorded, or 0 (the
+ * default parameters) if none was.  set: seeds it (e.g. replaying rank 0's tuned choice on every rank);
+ * CONV2D_ERR_INVALID_PARAMS unless `variant` is one the auto-selector enumerates for `p` and `algo`.
+ * `algo` must be CONV2D_ALGO_IMPLICIT_GEMM or CONV2D_ALGO_MATMUL_1X1 (CONV2D_ERR_INVALID_PARAMS
+ * otherwise; CONV2D_ERR_UNSUPPORTED if it cannot run `p`).  Host-only. */
+conv2d_status_t conv2d_get_variant(const conv2d_params_t* p, conv2d_algo_t algo, int* variant);
+conv2d_status_t conv2d_set_variant(const conv2d_params_t* p, conv2d_algo_t algo, int variant);
+
 /* Drop every cached choice. */
 void conv2d_clear_selection_cache(void);
 

@@ -41,7 +41,8 @@ EXPORTED = ["conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv
             "conv2d_clear_selection_cache", "conv2d_last_tune_times", "conv2d_launch_count",
             "conv2d_synth_fill", "conv2d_status_string", "conv2d_algo_name", "conv2d_last_error",
             "conv2d_debug_trace", "conv2d_save_selection", "conv2d_load_selection",
-            "pool2d_output_shape", "pool2d_forward", "conv2d_set_autotune_flush"]
+            "pool2d_output_shape", "pool2d_forward", "conv2d_set_autotune_flush", "conv2d_get_variant",
+            "conv2d_set_variant"]
 
 
 class conv2d_params_t(ctypes.Structure):
@@ -67,6 +68,8 @@ _lib.conv2d_forward.argtypes = [_P, ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_s
 _lib.conv2d_autotune.argtypes = [_P, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp, ctypes.POINTER(ctypes.c_int)]
 _lib.conv2d_selected.argtypes = [_P, ctypes.POINTER(ctypes.c_int)]
 _lib.conv2d_set_selected.argtypes = [_P, ctypes.c_int]
+_lib.conv2d_get_variant.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+_lib.conv2d_set_variant.argtypes = [_P, ctypes.c_int, ctypes.c_int]
 _lib.conv2d_clear_selection_cache.argtypes = []
 _lib.conv2d_clear_selection_cache.restype = None
 _lib.conv2d_last_tune_times.argtypes = [ctypes.POINTER(ctypes.c_double)]
@@ -227,6 +230,17 @@ def conv2d_selected(p: Params):
 
 def conv2d_set_selected(p: Params, algo: int) -> None:
     _check(_lib.conv2d_set_selected(ctypes.byref(p.c()), int(algo)), "conv2d_set_selected")
+
+
+def conv2d_get_variant(p: Params, algo: int) -> int:
+    """Tuned parameter variant of implicit_gemm / matmul_1x1 for p (0 = defaults; include/conv2d.h)."""
+    v = ctypes.c_int()
+    _check(_lib.conv2d_get_variant(ctypes.byref(p.c()), int(algo), ctypes.byref(v)), "conv2d_get_variant")
+    return int(v.value)
+
+
+def conv2d_set_variant(p: Params, algo: int, variant: int) -> None:
+    _check(_lib.conv2d_set_variant(ctypes.byref(p.c()), int(algo), int(variant)), "conv2d_set_variant")
 
 
 def conv2d_clear_selection_cache() -> None:

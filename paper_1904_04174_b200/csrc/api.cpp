@@ -420,6 +420,41 @@ conv2d_status_t conv2d_set_selected(const conv2d_params_t* p, conv2d_algo_t algo
   return CONV2D_OK;
 }
 
+static conv2d_status_t variant_problem(const conv2d_params_t* p, conv2d_algo_t algo, Problem* q) {
+  std::string why;
+  if (!shape_of(p, q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
+  if (algo != CONV2D_ALGO_IMPLICIT_GEMM && algo != CONV2D_ALGO_MATMUL_1X1)
+    return fail(CONV2D_ERR_INVALID_PARAMS, "variants exist for implicit_gemm / matmul_1x1 only");
+  if (!algo_supports(*q, algo)) return fail(CONV2D_ERR_UNSUPPORTED, "algorithm does not support these params");
+  return CONV2D_OK;
+}
+
+conv2d_status_t conv2d_get_variant(const conv2d_params_t* p, conv2d_algo_t algo, int* variant) {
+  if (!variant) return fail(CONV2D_ERR_NULL, "variant is NULL");
+  *variant = 0;
+  Problem q;
+  const conv2d_status_t st = variant_problem(p, algo, &q);
+  if (st != CONV2D_OK) return st;
+  int v = 0;
+  if (igemm_get_variant(q, algo == CONV2D_ALGO_MATMUL_1X1, &v)) *variant = v;
+  return CONV2D_OK;
+}
+
+conv2d_status_t conv2d_set_variant(const conv2d_params_t* p, conv2d_algo_t algo, int variant) {
+  Problem q;
+  const conv2d_status_t st = variant_problem(p, algo, &q);
+  if (st != CONV2D_OK) return st;
+  const bool is_1x1 = algo == CONV2D_ALGO_MATMUL_1X1;
+  int masks[32];
+  const int n = igemm_variants(q, is_1x1, masks);
+  for (int i = 0; i < n; ++i)
+    if (masks[i] == variant) {
+      igemm_set_variant(q, is_1x1, variant);
+      return CONV2D_OK;
+    }
+  return fail(CONV2D_ERR_INVALID_PARAMS, "variant " + std::to_string(variant) + " is not enumerated for these params");
+}
+
 // ---- persisted selector table (SPEC.md:354's line format, with the full key of this library's cache)
 //   N H W C F KH KW SH SW same|valid fp32|tf32 : algo[/variant]
 //   default : algo,algo,...        (ranking by win count over the entries; informative)

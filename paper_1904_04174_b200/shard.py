@@ -2,8 +2,8 @@
 
 Images are independent, so rank r of `world` owns the contiguous global images
 [r*B/world, (r+1)*B/world).  Nothing is exchanged on the data path; the collectives below are
-off the timed path: a broadcast of rank 0's per-layer algorithm choices (so every rank runs
-the same kernels) and a MAX reduction of per-rank device times (value = total work / max time).
+off the timed path: a broadcast of rank 0's per-layer algorithm choices and tuned variants (so every
+rank runs the same kernels) and a MAX reduction of per-rank device times (value = total work / max time).
 Backend-agnostic: used with NCCL by bench.py and with gloo by tests/test_shard_gloo.py.
 """
 from __future__ import annotations
@@ -20,14 +20,20 @@ def shard_range(global_batch: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def broadcast_choices(choices: dict, dist, device) -> dict:
-    """Rank 0's {layer name: algo id} wins on every rank (sorted-key order is the wire format)."""
+    """Rank 0's {layer name: choice} wins on every rank; a choice is an int (algorithm id) or a tuple
+    of ints (algorithm id, tuned parameter variant).  Wire format: one int32 row per sorted key."""
     import torch
     if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
         return dict(choices)
     names = sorted(choices)
-    t = torch.tensor([int(choices[k]) for k in names], dtype=torch.int32, device=device)
+    rows = [tuple(v) if isinstance(v, (tuple, list)) else (int(v),) for v in (choices[k] for k in names)]
+    width = len(rows[0]) if rows else 1
+    if any(len(r) != width for r in rows):
+        raise ValueError("choices must all have the same arity")
+    t = torch.tensor(rows, dtype=torch.int32, device=device).reshape(len(names), width)
     dist.broadcast(t, 0)
-    return dict(zip(names, (int(v) for v in t.tolist())))
+    vals = [tuple(int(x) for x in r) for r in t.tolist()]
+    return dict(zip(names, (v if width > 1 else v[0] for v in vals)))
 
 
 def max_over_ranks(value: float, dist, device) -> float:

@@ -159,6 +159,25 @@ def test_selection_cache_host_side(C):
     assert C.conv2d_selected(p) is None
 
 
+def test_variant_get_set_host_side(C):
+    """conv2d_get_variant / conv2d_set_variant (bench.py replays rank 0's tuned variants on every rank)."""
+    p = C.Params(3, 40, 40, 64, 64, 3, 3)  # 3x3/s1: halo and im2col A paths (bit 0) both enumerated
+    C.conv2d_set_variant(p, C.ALGO_IMPLICIT_GEMM, 1)
+    assert C.conv2d_get_variant(p, C.ALGO_IMPLICIT_GEMM) == 1
+    C.conv2d_set_variant(p, C.ALGO_IMPLICIT_GEMM, 0)
+    assert C.conv2d_get_variant(p, C.ALGO_IMPLICIT_GEMM) == 0
+    for bad in (4, 32, -1):  # bit 2 (LSU epilogue) is never enumerated; out of range
+        with pytest.raises(C.Conv2dError) as e:
+            C.conv2d_set_variant(p, C.ALGO_IMPLICIT_GEMM, bad)
+        assert e.value.status == C.ERR_INVALID_PARAMS
+    with pytest.raises(C.Conv2dError) as e:
+        C.conv2d_get_variant(p, C.ALGO_TILED)
+    assert e.value.status == C.ERR_INVALID_PARAMS
+    with pytest.raises(C.Conv2dError) as e:  # a 3x3 window is not a 1x1 matmul
+        C.conv2d_set_variant(p, C.ALGO_MATMUL_1X1, 0)
+    assert e.value.status == C.ERR_UNSUPPORTED
+
+
 @pytest.mark.parametrize("case", [(2, 13, 11, 5, 3, 3, 2, 2, 0), (256, 112, 112, 64, 3, 3, 2, 2, 0),
                                   (3, 14, 14, 4, 2, 2, 2, 2, 1), (1, 9, 10, 3, 4, 2, 3, 1, 0),
                                   (32, 7, 7, 2048, 7, 7, 1, 1, 1)], ids=str)

@@ -4,7 +4,7 @@ Each rank takes its batch shard with the same helpers bench.py uses (shard.py), 
 its slice of the global seeded batch, computes it (the oracle stands in for the device conv
 here -- this test exercises the sharding, not the kernels), then:
   * the gathered shards equal the unsharded result bit for bit (P11 on the host path);
-  * rank 0's algorithm choices win on every rank (broadcast_choices);
+  * rank 0's algorithm choices (and tuned variants) win on every rank (broadcast_choices);
   * max_over_ranks returns the slowest rank's time.
 """
 import os
@@ -40,8 +40,9 @@ def _worker(rank, world, port, out):
         y = O.conv2d(O.Params(b1 - b0, H, W, C, F, K, K, S, S, O.SAME), x, w, threads=1)
         full = gather_shards(torch.from_numpy(y), dist)
         choices = broadcast_choices({"R4": 3 + rank, "R17": 4 - rank}, dist, "cpu")
+        pairs = broadcast_choices({"R4": (3 + rank, 17 * rank), "R17": (4 - rank, 8)}, dist, "cpu")
         tmax = max_over_ranks(10.0 + rank, dist, "cpu")
-        out[rank] = (full.numpy(), choices, tmax)
+        out[rank] = (full.numpy(), choices, pairs, tmax)
     finally:
         dist.destroy_process_group()
 
@@ -55,9 +56,10 @@ def test_two_rank_gloo_shard_gather_bitwise():
     wg = synth.filter_hwcf(K, K, C, F, layer_id=31)
     ref = O.conv2d(O.Params(GB, H, W, C, F, K, K, S, S, O.SAME), xg, wg, threads=1)
     for r in range(world):
-        full, choices, tmax = out[r]
+        full, choices, pairs, tmax = out[r]
         assert np.array_equal(full, ref)
         assert choices == {"R4": 3, "R17": 4}  # rank 0's
+        assert pairs == {"R4": (3, 0), "R17": (4, 8)}  # (algorithm, variant) pairs: rank 0's
         assert tmax == 11.0
 
 
