@@ -884,12 +884,8 @@ cudaError_t launch_t(const CUtensorMap& a, const CUtensorMap& bh, const CUtensor
                      const DevArgs& args, int clusters, cudaStream_t s) {
   using C_ = Cfg<BN, THREE_X, BRES, AMODE == A_STEM>;
   auto kern = gemm2sm_kernel<BN, THREE_X, AMODE, BRES>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  const cudaError_t e = smem_attr_once<gemm2sm_kernel<BN, THREE_X, AMODE, BRES>>(C_::SMEM);
+  if (e != cudaSuccess) return e;
   return launch_k(kern, dim3(2 * clusters), dim3(NTHREADS), C_::SMEM, s, a, bh, bl, dm, args);
 }
 

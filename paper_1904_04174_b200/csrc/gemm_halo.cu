@@ -467,12 +467,8 @@ cudaError_t launch_h(const CUtensorMap& x, const CUtensorMap& bh, const CUtensor
                      const CUtensorMap& dm, const HArgs& a, int clusters, cudaStream_t s) {
   using C_ = HCfg<BN, THREE_X, GEOM>;
   auto kern = halo_kernel<BN, THREE_X, GEOM>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  const cudaError_t e = smem_attr_once<halo_kernel<BN, THREE_X, GEOM>>(C_::SMEM);
+  if (e != cudaSuccess) return e;
   return launch_k(kern, dim3(2 * clusters), dim3(NTHREADS), C_::SMEM, s, x, bh, bhf, blf, dm, a);
 }
 

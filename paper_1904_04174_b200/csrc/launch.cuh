@@ -14,6 +14,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cstdint>
 #include <cstdlib>
 #include <utility>
 
@@ -25,6 +27,21 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 inline bool pdl_enabled() {
   static const bool on = getenv("CONV2D_PDL") != nullptr;
   return on;
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize for kernel KERN, set once per device (the attribute is a
+// per-device property, so a process driving several GPUs needs it on each); thread-safe.
+template <auto KERN>
+cudaError_t smem_attr_once(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? (uint64_t{1} << dev) : 0;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
 }
 
 template <typename... KArgs, typename... Args>

@@ -117,11 +117,9 @@ cudaError_t launch_tiled(const Problem& p, const float* in, const float* filt, f
   const int IH = (TH - 1) * p.SH + p.KH, IW = (TW - 1) * p.SW + p.KW;
   const size_t smem = sizeof(float) * ((((size_t)IH * IW * (CC + 1)) + 3) / 4 * 4 + (size_t)p.KH * p.KW * CC * FB);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  static bool attr_set = false;  // benign race: idempotent
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  {
+    const cudaError_t e = smem_attr_once<tiled_kernel>(227 * 1024);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const int fblocks = (p.F + FB - 1) / FB;
   dim3 grid((p.WO + TW - 1) / TW, (p.HO + TH - 1) / TH, (unsigned)(p.N * fblocks));
