@@ -108,7 +108,9 @@ conv2d_status_t conv2d_query_workspace(const conv2d_params_t* p, conv2d_algo_t a
 /* The forward pass.  in/filt/out/ws: device pointers (see Ownership).
  * ws_bytes must be >= conv2d_query_workspace(p, algo).  With AUTO on a cache
  * miss this tunes first (see conv2d_autotune: it SYNCHRONISES the stream and
- * uses out/ws as scratch), then runs the chosen algorithm. */
+ * uses out/ws as scratch), then runs the chosen algorithm.  Under stream capture
+ * an AUTO cache miss returns CONV2D_ERR_UNSUPPORTED without touching the stream
+ * (tune before capturing); a cached AUTO choice and concrete algorithms capture. */
 conv2d_status_t conv2d_forward(const conv2d_params_t* p, conv2d_algo_t algo, const float* in,
                                const float* filt, float* out, void* ws, size_t ws_bytes, void* stream);
 
@@ -116,7 +118,8 @@ conv2d_status_t conv2d_forward(const conv2d_params_t* p, conv2d_algo_t algo, con
  * time every supported algorithm on the caller's buffers (CUDA events, W warm-ups
  * then R reps, best-of-R), pick the argmin with ties broken by enum order, cache it
  * under (params incl. batch/padding/math, device), and write it to *chosen.
- * Synchronises `stream`.  ws must be sized for AUTO. */
+ * Synchronises `stream`.  ws must be sized for AUTO.  CONV2D_ERR_UNSUPPORTED if
+ * `stream` is being captured (tuning cannot be captured). */
 conv2d_status_t conv2d_autotune(const conv2d_params_t* p, const float* in, const float* filt, float* out,
                                 void* ws, size_t ws_bytes, void* stream, conv2d_algo_t* chosen);
 

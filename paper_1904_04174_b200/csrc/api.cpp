@@ -353,6 +353,8 @@ static conv2d_status_t validate_call(const conv2d_params_t* p, conv2d_algo_t alg
   return CONV2D_OK;
 }
 
+static conv2d_status_t refuse_if_capturing(cudaStream_t s);
+
 conv2d_status_t conv2d_forward(const conv2d_params_t* p, conv2d_algo_t algo, const float* in, const float* filt,
                                float* out, void* ws, size_t ws_bytes, void* stream) {
   Problem q;
@@ -374,11 +376,24 @@ conv2d_status_t conv2d_forward(const conv2d_params_t* p, conv2d_algo_t algo, con
       }
     }
     if (!hit) {
+      st = refuse_if_capturing(s);
+      if (st != CONV2D_OK) return st;
       st = autotune_impl(p, q, dev, in, filt, out, ws, s, &a);
       if (st != CONV2D_OK) return st;
     }
   }
   return run_algo(q, a, in, filt, out, ws, s);
+}
+
+// Tuning times and synchronises the stream, which a stream capture forbids (and the failed call would
+// invalidate the caller's capture): refuse up front instead.
+static conv2d_status_t refuse_if_capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+    return fail(CONV2D_ERR_UNSUPPORTED,
+                "auto-selection needs a cached choice while the stream is being captured: tune first "
+                "(conv2d_autotune / conv2d_load_selection / conv2d_set_selected)");
+  return CONV2D_OK;
 }
 
 conv2d_status_t conv2d_autotune(const conv2d_params_t* p, const float* in, const float* filt, float* out, void* ws,
@@ -388,6 +403,8 @@ conv2d_status_t conv2d_autotune(const conv2d_params_t* p, const float* in, const
   if (st != CONV2D_OK) return st;
   int dev = -1;
   st = check_device(&dev);
+  if (st != CONV2D_OK) return st;
+  st = refuse_if_capturing(static_cast<cudaStream_t>(stream));
   if (st != CONV2D_OK) return st;
   return autotune_impl(p, q, dev, in, filt, out, ws, static_cast<cudaStream_t>(stream), chosen);
 }

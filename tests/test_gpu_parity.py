@@ -201,6 +201,39 @@ def test_autotune_and_auto_forward(cuda_ok):
     assert c.conv2d_selected(p2) is not None
 
 
+def test_auto_under_stream_capture(cuda_ok):
+    """An AUTO cache miss inside a CUDA-graph capture is refused (tuning synchronises the stream) without
+    breaking the capture; once tuned, AUTO captures and replays to the oracle's result."""
+    import torch
+    c = C()
+    c.conv2d_clear_selection_cache()
+    p = P(2, 20, 20, 64, 96, 3, 3)
+    x, w = make_inputs(p, layer_id=610)
+    ref, den = O.conv2d(oparams(p), x, w, with_denom=True)
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    y = torch.full((2, 20, 20, 96), float("nan"), device="cuda")
+    need = c.conv2d_query_workspace(p, c.ALGO_AUTO)
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+        with pytest.raises(c.Conv2dError) as e:
+            c.conv2d_forward(p, c.ALGO_AUTO, xd, wd, y, ws, need, s)
+        assert e.value.status == c.ERR_UNSUPPORTED
+        with pytest.raises(c.Conv2dError):
+            c.conv2d_autotune(p, xd, wd, y, ws, need, s)
+    assert c.conv2d_selected(p) is None
+    c.conv2d_autotune(p, xd, wd, y, ws, need)  # outside the capture
+    g2 = torch.cuda.CUDAGraph()
+    y.fill_(float("nan"))
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g2, stream=s, capture_error_mode="thread_local"):
+        c.conv2d_forward(p, c.ALGO_AUTO, xd, wd, y, ws, need, s)
+    g2.replay()
+    torch.cuda.synchronize()
+    check_close(p, y.cpu().numpy(), ref, den, c.ALGO_AUTO, "auto captured")
+
+
 def test_device_synth_matches_host_generator(cuda_ok):
     import torch
     c = C()
