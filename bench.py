@@ -143,7 +143,7 @@ def cpu_baseline(target_s: float = 12.0):
     w1 = oracle_sample(1)
     t1 = run_oracle(w1, threads)
     flops1 = sum(f for *_, f in w1)
-    images = max(1, min(16, int(target_s / max(t1, 1e-3))))
+    images = max(1, min(48, int(target_s / max(t1, 1e-3))))  # 48 images: ~4 GB of host tensors
     if images > 1:
         wk = oracle_sample(images)
         t = run_oracle(wk, threads)
