@@ -158,7 +158,8 @@ conv2d_status_t conv2d_set_autotune_flush(void* buf, size_t bytes);
  * (variant = the tuned algorithm parameters of implicit_gemm / matmul_1x1, see igemm.cu), then
  * `default : a,b,...` (algorithms by number of entries won; informative) and `#` comments.
  * save: CONV2D_ERR_IO if the file cannot be written.  load: parses and validates every line first
- * (CONV2D_ERR_INVALID_PARAMS for malformed lines / unknown names / invalid params,
+ * (CONV2D_ERR_INVALID_PARAMS for malformed lines / unknown names / invalid params / a variant the
+ * auto-selector does not enumerate for that line's params,
  * CONV2D_ERR_UNSUPPORTED if an algorithm cannot run its params -- detail with file:line in
  * conv2d_last_error()); only a fully valid file is applied, seeding the cache (and variants) so
  * conv2d_forward(AUTO) uses the stored choices without tuning.  *loaded = entries applied (may be NULL).

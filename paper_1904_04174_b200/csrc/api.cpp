@@ -636,6 +636,17 @@ conv2d_status_t conv2d_load_selection(const char* path, int* loaded) {
       why = "a variant is only defined for implicit_gemm / matmul_1x1";
       break;
     }
+    if (e.variant >= 0) {  // only the variants the auto-selector enumerates for these params (as set_variant)
+      int masks[32];
+      const int n = igemm_variants(q, e.a == CONV2D_ALGO_MATMUL_1X1, masks);
+      bool found = false;
+      for (int i = 0; i < n; ++i) found = found || masks[i] == e.variant;
+      if (!found) {
+        st = CONV2D_ERR_INVALID_PARAMS;
+        why = "variant " + std::to_string(e.variant) + " is not enumerated for these params";
+        break;
+      }
+    }
     entries.push_back(e);
   }
   fclose(f);

@@ -54,7 +54,7 @@ def test_variants_comments_and_default_line(C, tmp_path):
     f = tmp_path / "v.txt"
     f.write_text("# tuned on a B200\n\n"
                  "256 56 56 64 256 1 1 1 1 same fp32 : matmul_1x1/10   # B path + N tile\n"
-                 "256 14 14 256 256 3 3 1 1 same fp32 : implicit_gemm/3\n"
+                 "256 14 14 256 256 3 3 1 1 same fp32 : implicit_gemm/10\n"
                  "default : implicit_gemm, matmul_1x1,winograd_f2x2_3x3,direct,tiled\n")
     assert C.conv2d_load_selection(str(f)) == 2
     P = C.Params
@@ -63,7 +63,7 @@ def test_variants_comments_and_default_line(C, tmp_path):
     C.conv2d_save_selection(str(g))
     out = g.read_text()
     assert "256 56 56 64 256 1 1 1 1 same fp32 : matmul_1x1/10" in out
-    assert "256 14 14 256 256 3 3 1 1 same fp32 : implicit_gemm/3" in out
+    assert "256 14 14 256 256 3 3 1 1 same fp32 : implicit_gemm/10" in out
 
 
 @pytest.mark.parametrize("body,status", [
@@ -77,6 +77,7 @@ def test_variants_comments_and_default_line(C, tmp_path):
     ("1 8 8 4 8 7 7 2 2 same fp32 : winograd_f2x2_3x3\n", "CONV2D_ERR_UNSUPPORTED"),      # incompatible
     ("1 8 8 4 8 3 3 1 1 same fp32 : direct/2\n", "CONV2D_ERR_INVALID_PARAMS"),            # variant on direct
     ("1 8 8 4 8 3 3 1 1 same fp32 : implicit_gemm/99\n", "CONV2D_ERR_INVALID_PARAMS"),    # variant range
+    ("256 56 56 64 256 1 1 1 1 same fp32 : matmul_1x1/4\n", "CONV2D_ERR_INVALID_PARAMS"),  # never enumerated
     ("default : direct,bogus\n", "CONV2D_ERR_INVALID_PARAMS"),
 ])
 def test_invalid_files_leave_the_cache_untouched(C, tmp_path, body, status):
