@@ -210,3 +210,14 @@ def test_autotune_flush_registration(C):
     assert "INVALID_PARAMS" in str(ei.value)
     C.conv2d_set_autotune_flush(4096, 1 << 20)  # registration only: never dereferenced on the host
     C.conv2d_set_autotune_flush(None)
+
+
+def test_binding_fails_loudly_without_the_library(tmp_path):
+    """No CPU or library fallback: with libconv2d.so absent, importing the binding raises."""
+    import subprocess
+    import sys
+    code = "import paper_1904_04174_b200.conv2d"
+    env = dict(os.environ, CONV2D_LIB=str(tmp_path / "absent" / "libconv2d.so"))
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True)
+    assert r.returncode != 0
+    assert "libconv2d.so not found" in r.stderr and "no fallback" in r.stderr
