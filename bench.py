@@ -135,7 +135,7 @@ def run_oracle(work, threads):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(target_s: float = 12.0):
+def cpu_baseline(target_s: float = 15.0):
     """The oracle as it stands, on this host's cores, over a bounded sample of the workload."""
     import oracle as O
     O.build()
@@ -143,7 +143,7 @@ def cpu_baseline(target_s: float = 12.0):
     w1 = oracle_sample(1)
     t1 = run_oracle(w1, threads)
     flops1 = sum(f for *_, f in w1)
-    images = max(1, min(48, int(target_s / max(t1, 1e-3))))  # 48 images: ~4 GB of host tensors
+    images = max(1, min(64, int(target_s / max(t1, 1e-3))))  # 64 images: ~5.6 GB of host tensors
     if images > 1:
         wk = oracle_sample(images)
         t = run_oracle(wk, threads)
