@@ -184,7 +184,8 @@ def workload_config(args, per_gpu):
     gb = getattr(args, "global_batch", GLOBAL_BATCH)
     return {"workload": "resnet50_v1.5_conv_stack (53 convs, BASELINE configs[4])", "global_batch": gb,
             "per_gpu_batch": per_gpu, "math": "3xtf32 (fp32-faithful)" if args.math == "fp32" else "tf32",
-            "algo": "auto (measured per layer)", "parallelism": f"batch-shard x{args.gpus}",
+            "algo": ("auto (learned selector, conv2d_predict)" if getattr(args, "predict", False)
+                     else "auto (measured per layer)"), "parallelism": f"batch-shard x{args.gpus}",
             "l2": "flushed before every step (256 MiB write, outside the timed events); step working set ~22 GB",
             "gflop_per_step": round(sum(l.flops(gb) for _, l in L.resnet50_v15_stack()) / 1e9, 3)}
 
@@ -244,6 +245,8 @@ def main():
                     help="analysis only (default = BASELINE config 5's 256)")
     ap.add_argument("--layers-out", default="", help="write the per-layer table (JSON) here")
     ap.add_argument("--save-selection", default="", help="write the tuned selector table here (rank 0)")
+    ap.add_argument("--predict", action="store_true",
+                    help="take the learned selector's choices (conv2d_predict) instead of measuring (analysis)")
     ap.add_argument("--load-selection", default="", help="seed the selector from this table instead of tuning")
     ap.add_argument("--trace-out", default="", help="diagnostics: per-launch GEMM timeline of one extra "
                     "(untimed) graph replay of the step, JSON (include/conv2d_debug.h)")
@@ -305,6 +308,11 @@ def main():
         key = cv["layer"].name
         if key not in chosen:
             sel = C.conv2d_selected(cv["p"]) if args.load_selection else None
+            if sel is None and args.predict:  # the learned selector's choice, no measurement (conv2d_predict)
+                sel, v = C.conv2d_predict(cv["p"])
+                C.conv2d_set_selected(cv["p"], sel)
+                if sel in (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1):
+                    C.conv2d_set_variant(cv["p"], sel, v)
             chosen[key] = sel if sel is not None else C.conv2d_autotune(cv["p"], cv["x"], cv["w"], cv["y"], ws,
                                                                         ws.numel())
     if args.save_selection and rank == 0:

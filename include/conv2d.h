@@ -141,6 +141,20 @@ conv2d_status_t conv2d_set_selected(const conv2d_params_t* p, conv2d_algo_t algo
 conv2d_status_t conv2d_get_variant(const conv2d_params_t* p, conv2d_algo_t algo, int* variant);
 conv2d_status_t conv2d_set_variant(const conv2d_params_t* p, conv2d_algo_t algo, int variant);
 
+/* Learned selector (tuning decisions "are a good candidate for a learned
+ * solution rather than a hand tuned one"): the (algorithm, tuned variant) a decision tree trained on measured
+ * B200 timings predicts to be fastest for `p` -- features are shape quantities (log M, N, C, K, window,
+ * stride, padding, batch, math, tile count, arithmetic intensity); training data, cross-validated regret and
+ * the generator: tools/selector_data.py, tools/train_selector.py, profiles/data/selector_model_r1.json.
+ * Runs nothing on the device; the result always supports `p` (fallback implicit_gemm / 0). */
+conv2d_status_t conv2d_predict(const conv2d_params_t* p, conv2d_algo_t* algo, int* variant);
+
+/* What conv2d_forward(AUTO) does on a cache miss: MEASURE (default) tunes on the caller's buffers (see
+ * conv2d_autotune; refused under stream capture); PREDICT caches conv2d_predict's choice instead -- no
+ * timing, no synchronisation, so it also works inside a CUDA-graph capture.  Process-wide. */
+typedef enum { CONV2D_AUTO_MEASURE = 0, CONV2D_AUTO_PREDICT = 1 } conv2d_auto_policy_t;
+conv2d_status_t conv2d_set_auto_policy(conv2d_auto_policy_t policy);
+
 /* Drop every cached choice. */
 void conv2d_clear_selection_cache(void);
 

@@ -42,7 +42,7 @@ EXPORTED = ["conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv
             "conv2d_synth_fill", "conv2d_status_string", "conv2d_algo_name", "conv2d_last_error",
             "conv2d_debug_trace", "conv2d_save_selection", "conv2d_load_selection",
             "pool2d_output_shape", "pool2d_forward", "conv2d_set_autotune_flush", "conv2d_get_variant",
-            "conv2d_set_variant"]
+            "conv2d_set_variant", "conv2d_predict", "conv2d_set_auto_policy"]
 
 
 class conv2d_params_t(ctypes.Structure):
@@ -70,6 +70,8 @@ _lib.conv2d_selected.argtypes = [_P, ctypes.POINTER(ctypes.c_int)]
 _lib.conv2d_set_selected.argtypes = [_P, ctypes.c_int]
 _lib.conv2d_get_variant.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
 _lib.conv2d_set_variant.argtypes = [_P, ctypes.c_int, ctypes.c_int]
+_lib.conv2d_predict.argtypes = [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+_lib.conv2d_set_auto_policy.argtypes = [ctypes.c_int]
 _lib.conv2d_clear_selection_cache.argtypes = []
 _lib.conv2d_clear_selection_cache.restype = None
 _lib.conv2d_last_tune_times.argtypes = [ctypes.POINTER(ctypes.c_double)]
@@ -241,6 +243,20 @@ def conv2d_get_variant(p: Params, algo: int) -> int:
 
 def conv2d_set_variant(p: Params, algo: int, variant: int) -> None:
     _check(_lib.conv2d_set_variant(ctypes.byref(p.c()), int(algo), int(variant)), "conv2d_set_variant")
+
+
+AUTO_MEASURE, AUTO_PREDICT = 0, 1
+
+
+def conv2d_predict(p: Params) -> tuple[int, int]:
+    """The learned selector's (algorithm, variant) for p (include/conv2d.h; runs nothing on the device)."""
+    a, v = ctypes.c_int(), ctypes.c_int()
+    _check(_lib.conv2d_predict(ctypes.byref(p.c()), ctypes.byref(a), ctypes.byref(v)), "conv2d_predict")
+    return int(a.value), int(v.value)
+
+
+def conv2d_set_auto_policy(policy: int) -> None:
+    _check(_lib.conv2d_set_auto_policy(int(policy)), "conv2d_set_auto_policy")
 
 
 def conv2d_clear_selection_cache() -> None:

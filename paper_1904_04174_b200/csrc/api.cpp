@@ -15,6 +15,8 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <atomic>
+#include <cmath>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -22,6 +24,7 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "selector_tree.h"
 #include "../../include/conv2d_debug.h"
 #include "../../include/pool2d.h"
 
@@ -285,6 +288,59 @@ bool valid_algo(conv2d_algo_t a) { return (int)a >= 0 && (int)a < CONV2D_NUM_ALG
 
 }  // namespace
 
+// ---- learned selector: evaluation of the tree in selector_tree.h.
+// Features in the order of tools/train_selector.py FEATURES (the two must stay in step; a CPU test walks the
+// exported tree in Python with that script's features and compares with conv2d_predict).
+static void selector_features(const conv2d_params_t* p, const Problem& q, double x[selector::kFeatures]) {
+  const double m = (double)q.N * q.HO * q.WO;
+  const double kk = (double)q.KH * q.KW * q.C;
+  const int bn = q.F <= 64 ? 64 : q.F <= 128 ? 128 : 256;
+  const double tiles = std::ceil(m / 256.0) * std::ceil((double)q.F / bn);
+  const double flops = 2.0 * m * q.F * kk;
+  const double bytes = 4.0 * ((double)q.N * q.H * q.W * q.C + kk * q.F + m * q.F);
+  const double f[selector::kFeatures] = {std::log2(m), std::log2((double)q.F), std::log2((double)q.C), std::log2(kk),
+                                         (double)q.KH, (double)q.SH, p->padding == CONV2D_PAD_VALID ? 1.0 : 0.0,
+                                         std::log2((double)q.N), std::log2((double)q.HO * q.WO),
+                                         q.math == CONV2D_MATH_TF32 ? 1.0 : 0.0, std::log2(tiles), std::log2(flops),
+                                         flops / bytes};
+  for (int i = 0; i < selector::kFeatures; ++i) x[i] = f[i];
+}
+
+static bool variant_enumerated(const Problem& q, conv2d_algo_t a, int v) {
+  if (a != CONV2D_ALGO_IMPLICIT_GEMM && a != CONV2D_ALGO_MATMUL_1X1) return v == 0;
+  int masks[32];
+  const int n = igemm_variants(q, a == CONV2D_ALGO_MATMUL_1X1, masks);
+  for (int i = 0; i < n; ++i)
+    if (masks[i] == v) return true;
+  return false;
+}
+
+// the supported candidate of least predicted log-regret at the shape's leaf (fallback: implicit_gemm/0)
+static void selector_predict(const conv2d_params_t* p, const Problem& q, conv2d_algo_t* algo, int* variant) {
+  double x[selector::kFeatures];
+  selector_features(p, q, x);
+  int node = 0;
+  while (selector::kFeature[node] >= 0)
+    node = x[selector::kFeature[node]] <= selector::kThreshold[node] ? selector::kLeft[node] : selector::kRight[node];
+  const float* lr = selector::kLogRegret[selector::kLeafRow[node]];
+  int order[selector::kClasses];
+  for (int i = 0; i < selector::kClasses; ++i) order[i] = i;
+  std::stable_sort(order, order + selector::kClasses, [&](int a, int b) { return lr[a] < lr[b]; });
+  *algo = CONV2D_ALGO_IMPLICIT_GEMM;
+  *variant = 0;
+  for (int i = 0; i < selector::kClasses; ++i) {
+    const conv2d_algo_t a = (conv2d_algo_t)selector::kClassAlgo[order[i]];
+    const int v = selector::kClassVariant[order[i]];
+    if (algo_supports(q, a) && variant_enumerated(q, a, v)) {
+      *algo = a;
+      *variant = v;
+      return;
+    }
+  }
+}
+
+static std::atomic<int> g_auto_policy{CONV2D_AUTO_MEASURE};
+
 extern "C" {
 
 conv2d_status_t conv2d_output_shape(const conv2d_params_t* p, int32_t out_nhwf[4], int32_t pads_tblr[4]) {
@@ -375,7 +431,13 @@ conv2d_status_t conv2d_forward(const conv2d_params_t* p, conv2d_algo_t algo, con
         hit = true;
       }
     }
-    if (!hit) {
+    if (!hit && g_auto_policy.load() == CONV2D_AUTO_PREDICT) {  // learned choice: no timing, capture-safe
+      int v = 0;
+      selector_predict(p, q, &a, &v);
+      if (a == CONV2D_ALGO_IMPLICIT_GEMM || a == CONV2D_ALGO_MATMUL_1X1) igemm_set_variant(q, a == CONV2D_ALGO_MATMUL_1X1, v);
+      std::lock_guard<std::mutex> lk(g_cache_mu);
+      g_cache[key_of(p, dev)] = a;
+    } else if (!hit) {
       st = refuse_if_capturing(s);
       if (st != CONV2D_OK) return st;
       st = autotune_impl(p, q, dev, in, filt, out, ws, s, &a);
@@ -470,6 +532,22 @@ conv2d_status_t conv2d_set_variant(const conv2d_params_t* p, conv2d_algo_t algo,
       return CONV2D_OK;
     }
   return fail(CONV2D_ERR_INVALID_PARAMS, "variant " + std::to_string(variant) + " is not enumerated for these params");
+}
+
+conv2d_status_t conv2d_predict(const conv2d_params_t* p, conv2d_algo_t* algo, int* variant) {
+  if (!algo || !variant) return fail(CONV2D_ERR_NULL, "algo / variant is NULL");
+  Problem q;
+  std::string why;
+  if (!shape_of(p, &q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
+  selector_predict(p, q, algo, variant);
+  return CONV2D_OK;
+}
+
+conv2d_status_t conv2d_set_auto_policy(conv2d_auto_policy_t policy) {
+  if (policy != CONV2D_AUTO_MEASURE && policy != CONV2D_AUTO_PREDICT)
+    return fail(CONV2D_ERR_INVALID_PARAMS, "unknown auto policy");
+  g_auto_policy.store(policy);
+  return CONV2D_OK;
 }
 
 // ---- persisted selector table (SPEC.md:354's line format, with the full key of this library's cache)

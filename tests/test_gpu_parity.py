@@ -235,6 +235,37 @@ def test_auto_under_stream_capture(cuda_ok):
     check_close(p, y.cpu().numpy(), ref, den, c.ALGO_AUTO, "auto captured")
 
 
+def test_auto_predict_policy_captures(cuda_ok):
+    """CONV2D_AUTO_PREDICT: an AUTO cache miss takes the learned selector's choice (no timing, no sync), so
+    it captures into a CUDA graph; the replay matches the oracle and the cached choice is the prediction."""
+    import torch
+    c = C()
+    c.conv2d_clear_selection_cache()
+    p = P(3, 18, 22, 64, 128, 3, 3)
+    x, w = make_inputs(p, layer_id=620)
+    ref, den = O.conv2d(oparams(p), x, w, with_denom=True)
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    (n, ho, wo, f), _ = c.conv2d_output_shape(p)
+    y = torch.full((n, ho, wo, f), float("nan"), device="cuda")
+    need = c.conv2d_query_workspace(p, c.ALGO_AUTO)
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    c.conv2d_set_auto_policy(c.AUTO_PREDICT)
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s, capture_error_mode="thread_local"):
+            c.conv2d_forward(p, c.ALGO_AUTO, xd, wd, y, ws, need, s)
+        g.replay()
+        torch.cuda.synchronize()
+    finally:
+        c.conv2d_set_auto_policy(c.AUTO_MEASURE)
+    a, v = c.conv2d_predict(p)
+    assert c.conv2d_selected(p) == a
+    if a in (c.ALGO_IMPLICIT_GEMM, c.ALGO_MATMUL_1X1):
+        assert c.conv2d_get_variant(p, a) == v
+    check_close(p, y.cpu().numpy(), ref, den, c.ALGO_AUTO, "auto predict captured")
+
+
 def test_device_synth_matches_host_generator(cuda_ok):
     import torch
     c = C()
