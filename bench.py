@@ -185,6 +185,7 @@ def workload_config(args, per_gpu):
     return {"workload": "resnet50_v1.5_conv_stack (53 convs, BASELINE configs[4])", "global_batch": gb,
             "per_gpu_batch": per_gpu, "math": "3xtf32 (fp32-faithful)" if args.math == "fp32" else "tf32",
             "algo": ("auto (learned selector, conv2d_predict)" if getattr(args, "predict", False)
+                     else "auto (measured: learned top-3 candidates)" if getattr(args, "hybrid", False)
                      else "auto (measured per layer)"), "parallelism": f"batch-shard x{args.gpus}",
             "l2": "flushed before every step (256 MiB write, outside the timed events); step working set ~22 GB",
             "gflop_per_step": round(sum(l.flops(gb) for _, l in L.resnet50_v15_stack()) / 1e9, 3)}
@@ -245,6 +246,8 @@ def main():
                     help="analysis only (default = BASELINE config 5's 256)")
     ap.add_argument("--layers-out", default="", help="write the per-layer table (JSON) here")
     ap.add_argument("--save-selection", default="", help="write the tuned selector table here (rank 0)")
+    ap.add_argument("--hybrid", action="store_true",
+                    help="measure only the learned selector's top 3 candidates per layer (CONV2D_AUTO_HYBRID)")
     ap.add_argument("--predict", action="store_true",
                     help="take the learned selector's choices (conv2d_predict) instead of measuring (analysis)")
     ap.add_argument("--load-selection", default="", help="seed the selector from this table instead of tuning")
@@ -301,6 +304,9 @@ def main():
     # ---- auto-selection (measured, once per distinct layer); rank 0's choices (algorithm + tuned
     #      variant) broadcast so every rank runs the same kernels (off the timed path)
     chosen = {}
+    tune0 = time.perf_counter()
+    if args.hybrid:  # time only the learned selector's top candidates per layer (CONV2D_AUTO_HYBRID)
+        C.conv2d_set_auto_policy(C.AUTO_HYBRID)
     C.conv2d_set_autotune_flush(flush)  # cache-cold candidate timings, as in the timed step
     if args.load_selection:
         C.conv2d_load_selection(args.load_selection)
@@ -318,6 +324,8 @@ def main():
     if args.save_selection and rank == 0:
         C.conv2d_save_selection(args.save_selection)
     C.conv2d_set_autotune_flush(None)
+    C.conv2d_set_auto_policy(C.AUTO_MEASURE)
+    tune_s = time.perf_counter() - tune0
     gemm_like = (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1)
     chosen = {k: (a, C.conv2d_get_variant(next(cv["p"] for cv in convs if cv["layer"].name == k), a)
                   if a in gemm_like else 0) for k, a in chosen.items()}
@@ -523,7 +531,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 3), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32" if math == C.MATH_FP32 else "tf32",
                 "data": "synthetic (seeded splitmix64 uniform[-1,1), device-generated)",
-                "config": dict(workload_config(args, B), cuda_graph=graphs is not None),
+                "config": dict(workload_config(args, B), cuda_graph=graphs is not None,
+                               selection_s=round(tune_s, 2)),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "wall_s_timed": round(wall, 3),
                 "pct_of_peak": round(100 * value / 1e3 / (useful_peak * world), 2)}

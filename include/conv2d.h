@@ -151,8 +151,10 @@ conv2d_status_t conv2d_predict(const conv2d_params_t* p, conv2d_algo_t* algo, in
 
 /* What conv2d_forward(AUTO) does on a cache miss: MEASURE (default) tunes on the caller's buffers (see
  * conv2d_autotune; refused under stream capture); PREDICT caches conv2d_predict's choice instead -- no
- * timing, no synchronisation, so it also works inside a CUDA-graph capture.  Process-wide. */
-typedef enum { CONV2D_AUTO_MEASURE = 0, CONV2D_AUTO_PREDICT = 1 } conv2d_auto_policy_t;
+ * timing, no synchronisation, so it also works inside a CUDA-graph capture; HYBRID tunes like MEASURE
+ * (conv2d_autotune too) but times only the learned selector's top 3 candidates (CONV2D_HYBRID_TOPK).
+ * Process-wide. */
+typedef enum { CONV2D_AUTO_MEASURE = 0, CONV2D_AUTO_PREDICT = 1, CONV2D_AUTO_HYBRID = 2 } conv2d_auto_policy_t;
 conv2d_status_t conv2d_set_auto_policy(conv2d_auto_policy_t policy);
 
 /* Drop every cached choice. */

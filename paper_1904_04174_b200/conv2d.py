@@ -245,7 +245,7 @@ def conv2d_set_variant(p: Params, algo: int, variant: int) -> None:
     _check(_lib.conv2d_set_variant(ctypes.byref(p.c()), int(algo), int(variant)), "conv2d_set_variant")
 
 
-AUTO_MEASURE, AUTO_PREDICT = 0, 1
+AUTO_MEASURE, AUTO_PREDICT, AUTO_HYBRID = 0, 1, 2
 
 
 def conv2d_predict(p: Params) -> tuple[int, int]:

@@ -197,6 +197,11 @@ std::mutex g_flush_mu;
 void* g_flush_buf = nullptr;
 size_t g_flush_bytes = 0;
 
+// learned-selector ranking (defined with the selector below): the first `k` runnable (algorithm, variant)
+// candidates for q in order of predicted log-regret; returns how many were written
+int selector_topk(const conv2d_params_t* p, const Problem& q, int k, int* algos, int* variants);
+int auto_policy();
+
 conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int dev, const float* in, const float* filt,
                               float* out, void* ws, cudaStream_t s, conv2d_algo_t* chosen) {
   const int warm = std::max(1, env_int("CONV2D_AUTOTUNE_WARMUPS", 2));
@@ -220,6 +225,16 @@ conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int de
   conv2d_algo_t best = CONV2D_ALGO_AUTO;
   double best_t = 1e300;
   conv2d_status_t st = CONV2D_OK;
+  // CONV2D_AUTO_HYBRID: time only the learned selector's top candidates (default 3)
+  int top_a[32], top_v[32], ntop = 0;
+  const bool hybrid = auto_policy() == CONV2D_AUTO_HYBRID;
+  if (hybrid) ntop = selector_topk(p, q, std::min(32, std::max(1, env_int("CONV2D_HYBRID_TOPK", 3))), top_a, top_v);
+  auto measured = [&](int a, int v) {
+    if (!hybrid) return true;
+    for (int i = 0; i < ntop; ++i)
+      if (top_a[i] == a && top_v[i] == v) return true;
+    return false;
+  };
   for (int ai = 1; ai < CONV2D_NUM_ALGOS && st == CONV2D_OK; ++ai) {
     const conv2d_algo_t a = (conv2d_algo_t)ai;
     if (!algo_supports(q, a)) continue;
@@ -232,6 +247,7 @@ conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int de
     int v_best = 0;
     for (int vi = 0; vi < nvar && st == CONV2D_OK; ++vi) {
       const int v = masks[vi];
+      if (!measured(ai, v)) continue;
       if (gemm_like) igemm_set_variant(q, is_1x1, v);
       for (int w = 0; w < warm && st == CONV2D_OK; ++w) st = run_algo(q, a, in, filt, out, ws, s);
       for (int r = 0; r < reps && st == CONV2D_OK; ++r) {
@@ -259,6 +275,7 @@ conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int de
       }
     }
     if (st != CONV2D_OK) break;
+    if (t_best >= 1e299) continue;  // hybrid: no variant of this algorithm was timed
     if (gemm_like) igemm_set_variant(q, is_1x1, v_best);
     g_tune_times[ai] = t_best * 1000.0;
     if (t_best < best_t) {  // strict: ties keep the earlier enum
@@ -316,7 +333,12 @@ static bool variant_enumerated(const Problem& q, conv2d_algo_t a, int v) {
 }
 
 // the supported candidate of least predicted log-regret at the shape's leaf (fallback: implicit_gemm/0)
-static void selector_predict(const conv2d_params_t* p, const Problem& q, conv2d_algo_t* algo, int* variant) {
+static std::atomic<int> g_auto_policy{CONV2D_AUTO_MEASURE};
+
+namespace {
+int auto_policy() { return g_auto_policy.load(); }
+
+int selector_topk(const conv2d_params_t* p, const Problem& q, int k, int* algos, int* variants) {
   double x[selector::kFeatures];
   selector_features(p, q, x);
   int node = 0;
@@ -326,20 +348,31 @@ static void selector_predict(const conv2d_params_t* p, const Problem& q, conv2d_
   int order[selector::kClasses];
   for (int i = 0; i < selector::kClasses; ++i) order[i] = i;
   std::stable_sort(order, order + selector::kClasses, [&](int a, int b) { return lr[a] < lr[b]; });
-  *algo = CONV2D_ALGO_IMPLICIT_GEMM;
-  *variant = 0;
-  for (int i = 0; i < selector::kClasses; ++i) {
+  int n = 0;
+  for (int i = 0; i < selector::kClasses && n < k; ++i) {
     const conv2d_algo_t a = (conv2d_algo_t)selector::kClassAlgo[order[i]];
     const int v = selector::kClassVariant[order[i]];
     if (algo_supports(q, a) && variant_enumerated(q, a, v)) {
-      *algo = a;
-      *variant = v;
-      return;
+      algos[n] = a;
+      variants[n] = v;
+      ++n;
     }
   }
+  if (n == 0) {  // nothing runnable ranked: implicit_gemm / 0 always is
+    algos[0] = CONV2D_ALGO_IMPLICIT_GEMM;
+    variants[0] = 0;
+    n = 1;
+  }
+  return n;
 }
+}  // namespace
 
-static std::atomic<int> g_auto_policy{CONV2D_AUTO_MEASURE};
+static void selector_predict(const conv2d_params_t* p, const Problem& q, conv2d_algo_t* algo, int* variant) {
+  int a = 0, v = 0;
+  selector_topk(p, q, 1, &a, &v);
+  *algo = (conv2d_algo_t)a;
+  *variant = v;
+}
 
 extern "C" {
 
@@ -544,7 +577,7 @@ conv2d_status_t conv2d_predict(const conv2d_params_t* p, conv2d_algo_t* algo, in
 }
 
 conv2d_status_t conv2d_set_auto_policy(conv2d_auto_policy_t policy) {
-  if (policy != CONV2D_AUTO_MEASURE && policy != CONV2D_AUTO_PREDICT)
+  if (policy != CONV2D_AUTO_MEASURE && policy != CONV2D_AUTO_PREDICT && policy != CONV2D_AUTO_HYBRID)
     return fail(CONV2D_ERR_INVALID_PARAMS, "unknown auto policy");
   g_auto_policy.store(policy);
   return CONV2D_OK;

@@ -266,6 +266,35 @@ def test_auto_predict_policy_captures(cuda_ok):
     check_close(p, y.cpu().numpy(), ref, den, c.ALGO_AUTO, "auto predict captured")
 
 
+def test_auto_hybrid_policy_times_top_candidates(cuda_ok):
+    """CONV2D_AUTO_HYBRID: conv2d_autotune times only the learned selector's top 3 candidates -- at most three
+    algorithms report times, the prediction among them -- and the chosen algorithm is correct."""
+    import torch
+    c = C()
+    c.conv2d_clear_selection_cache()
+    p = P(2, 24, 24, 64, 96, 3, 3)
+    x, w = make_inputs(p, layer_id=630)
+    ref, den = O.conv2d(oparams(p), x, w, with_denom=True)
+    xd, wd = torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda()
+    (n, ho, wo, f), _ = c.conv2d_output_shape(p)
+    y = torch.empty((n, ho, wo, f), device="cuda")
+    need = c.conv2d_query_workspace(p, c.ALGO_AUTO)
+    ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+    c.conv2d_set_auto_policy(c.AUTO_HYBRID)
+    try:
+        a = c.conv2d_autotune(p, xd, wd, y, ws, need)
+        times = c.conv2d_last_tune_times()
+    finally:
+        c.conv2d_set_auto_policy(c.AUTO_MEASURE)
+    assert 1 <= len(times) <= 3
+    assert c.ALGO_NAMES[c.conv2d_predict(p)[0]] in times
+    assert c.ALGO_NAMES[a] in times
+    y.fill_(float("nan"))
+    c.conv2d_forward(p, c.ALGO_AUTO, xd, wd, y, ws, need)
+    torch.cuda.synchronize()
+    check_close(p, y.cpu().numpy(), ref, den, c.ALGO_AUTO, "auto hybrid")
+
+
 def test_device_synth_matches_host_generator(cuda_ok):
     import torch
     c = C()

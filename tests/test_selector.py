@@ -130,4 +130,5 @@ def test_replayed_regret_on_measured_shapes(C):
 def test_auto_policy_validation(C):
     with pytest.raises(C.Conv2dError):
         C.conv2d_set_auto_policy(7)
-    C.conv2d_set_auto_policy(C.AUTO_MEASURE)
+    for pol in (C.AUTO_PREDICT, C.AUTO_HYBRID, C.AUTO_MEASURE):
+        C.conv2d_set_auto_policy(pol)
