@@ -24,6 +24,7 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "launch.cuh"
 #include "selector_tree.h"
 #include "../../include/conv2d_debug.h"
 #include "../../include/pool2d.h"
@@ -173,6 +174,11 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 conv2d_status_t run_algo(const Problem& q, conv2d_algo_t a, const float* in, const float* filt, float* out, void* ws,
                          cudaStream_t s) {
   cudaError_t e = cudaSuccess;
+  struct PdlHint {  // launch.cuh: programmatic dependent launch for small convs
+    explicit PdlHint(bool on) { t_pdl_hint = on; }
+    ~PdlHint() { t_pdl_hint = false; }
+  } hint(2.0 * (double)q.M() * q.F * (double)q.K() <= 8e9 &&
+         ((q.M() + 255) / 256) * ((q.F + (q.F <= 64 ? 63 : q.F <= 128 ? 127 : 255)) / (q.F <= 64 ? 64 : q.F <= 128 ? 128 : 256)) <= 1024);
   switch (a) {
     case CONV2D_ALGO_DIRECT: e = launch_direct(q, in, filt, out, s); break;
     case CONV2D_ALGO_TILED: e = launch_tiled(q, in, filt, out, s); break;

@@ -7,10 +7,9 @@
 //   * pdl_wait() before its first global-memory read or write: returns once the previous grid has
 //     completed and its writes are visible.  Since every kernel waits before it can complete, kernel
 //     i+1 completing implies kernel i completed -- stream order stays transitive.
-// Opt-in (CONV2D_PDL=1): measured on the 53-conv step it changes nothing beyond noise (b32 -0.5%,
-// b256 +0.4%) -- the wait releases only after the previous grid's completion flush, which is most of
-// the ~1.4 us kernel-to-kernel gap inside a CUDA graph, and early-launched waiting CTAs interleave
-// with the tail of the chain.  Without the attribute griddepcontrol.* are no-ops.
+// Size-gated (pdl_enabled below): small convs only.  The wait releases only after the previous grid's
+// completion flush, so the gain is the launch + prologue of CTAs that land on SMs the previous grid's
+// tail has already freed.  Without the attribute griddepcontrol.* are no-ops.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -24,9 +23,15 @@ namespace conv2d {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Set by run_algo around the launches of one conv2d_forward: the conv is small (<= 8 GFLOP and <= 1024
+// pair tiles, i.e. a few waves), so its launch + prologue are worth overlapping with the previous tail.
+inline thread_local bool t_pdl_hint = false;
+
+// PDL on a launch: CONV2D_PDL=1 always, CONV2D_PDL=0 never, unset: for small convs (t_pdl_hint).
+// Measured (same box, fixed selection): b32 step -1.3% with PDL, b256 +1.1% -- hence size-gated.
 inline bool pdl_enabled() {
-  static const bool on = getenv("CONV2D_PDL") != nullptr;
-  return on;
+  static const int mode = getenv("CONV2D_PDL") ? atoi(getenv("CONV2D_PDL")) : -1;
+  return mode >= 0 ? mode == 1 : t_pdl_hint;
 }
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize for kernel KERN, set once per device (the attribute is a
