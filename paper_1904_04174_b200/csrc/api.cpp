@@ -178,7 +178,7 @@ conv2d_status_t run_algo(const Problem& q, conv2d_algo_t a, const float* in, con
     explicit PdlHint(bool on) { t_pdl_hint = on; }
     ~PdlHint() { t_pdl_hint = false; }
   } hint(2.0 * (double)q.M() * q.F * (double)q.K() <= 8e9 &&
-         ((q.M() + 255) / 256) * ((q.F + (q.F <= 64 ? 63 : q.F <= 128 ? 127 : 255)) / (q.F <= 64 ? 64 : q.F <= 128 ? 128 : 256)) <= 1024);
+         ((q.M() + 255) / 256) * ((q.F + (q.F <= 64 ? 63 : q.F <= 128 ? 127 : 255)) / (q.F <= 64 ? 64 : q.F <= 128 ? 128 : 256)) <= 2048);
   switch (a) {
     case CONV2D_ALGO_DIRECT: e = launch_direct(q, in, filt, out, s); break;
     case CONV2D_ALGO_TILED: e = launch_tiled(q, in, filt, out, s); break;

@@ -23,12 +23,12 @@ namespace conv2d {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-// Set by run_algo around the launches of one conv2d_forward: the conv is small (<= 8 GFLOP and <= 1024
+// Set by run_algo around the launches of one conv2d_forward: the conv is small (<= 8 GFLOP and <= 2048
 // pair tiles, i.e. a few waves), so its launch + prologue are worth overlapping with the previous tail.
 inline thread_local bool t_pdl_hint = false;
 
 // PDL on a launch: CONV2D_PDL=1 always, CONV2D_PDL=0 never, unset: for small convs (t_pdl_hint).
-// Measured (same box, fixed selection): b32 step -1.3% with PDL, b256 +1.1% -- hence size-gated.
+// Measured (same box, fixed selection): on every launch b32 -1.3%, b256 +1.1%; size-gated b32 -1.3%, b256 0.
 inline bool pdl_enabled() {
   static const int mode = getenv("CONV2D_PDL") ? atoi(getenv("CONV2D_PDL")) : -1;
   return mode >= 0 ? mode == 1 : t_pdl_hint;
