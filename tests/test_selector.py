@@ -132,3 +132,18 @@ def test_auto_policy_validation(C):
         C.conv2d_set_auto_policy(7)
     for pol in (C.AUTO_PREDICT, C.AUTO_HYBRID, C.AUTO_MEASURE):
         C.conv2d_set_auto_policy(pol)
+
+
+def test_committed_tree_is_reproducible_from_committed_data(tmp_path):
+    """selector_tree.h is exactly what tools/train_selector.py fits to profiles/data/selector_data_r1*.json (the
+    depth the committed header states, no cross-validation needed): the compiled model has a provenance."""
+    import subprocess
+    import sys
+    src = open(HEADER).read()
+    depth = int(re.search(r"depth (\d+), \d+ nodes", src).group(1))
+    out = tmp_path / "tree.h"
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "train_selector.py"), *DATA, "--depth", str(depth),
+                        "--no-cv", "--header", str(out)], capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    strip = lambda s: "\n".join(l for l in s.splitlines() if not l.startswith("//"))  # noqa: E731
+    assert strip(out.read_text()) == strip(src)

@@ -64,6 +64,8 @@ def main():
     ap.add_argument("--header", default="")
     ap.add_argument("--report", default="")
     ap.add_argument("--leaf", type=int, default=2, help="min samples per leaf")
+    ap.add_argument("--depth", type=int, default=0, help="fixed tree depth (skips the depth search)")
+    ap.add_argument("--no-cv", action="store_true", help="fit only (no cross-validation; with --depth)")
     args = ap.parse_args()
     from sklearn.model_selection import KFold
     from sklearn.tree import DecisionTreeRegressor
@@ -92,9 +94,9 @@ def main():
     wts = tbest / tbest.mean()
     kf = KFold(5, shuffle=True, random_state=0)
     cv = {}
-    for depth in (4, 6, 8, 10, 12, 16):
-        regs = np.zeros(len(rows))
-        for tr, te in kf.split(X):
+    for depth in ((args.depth,) if args.depth else (4, 6, 8, 10, 12, 16)):
+        regs = np.ones(len(rows))
+        for tr, te in ([] if args.no_cv else kf.split(X)):
             m = DecisionTreeRegressor(max_depth=depth, min_samples_leaf=args.leaf, random_state=0).fit(
                 X[tr], Y[tr], sample_weight=wts[tr])
             P = m.predict(X[te])
