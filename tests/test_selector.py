@@ -19,7 +19,8 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "paper_1904_04174_b200", "csrc", "selector_tree.h")
-DATA = [os.path.join(ROOT, "profiles", "data", f) for f in ("selector_data_r1.json", "selector_data_r1b.json")]
+DATA = [os.path.join(ROOT, "profiles", "data", f)
+        for f in ("selector_data_r1.json", "selector_data_r1b.json", "selector_data_r1c.json")]
 
 
 @pytest.fixture(scope="module")
