@@ -141,10 +141,11 @@ def test_committed_tree_is_reproducible_from_committed_data(tmp_path):
     import subprocess
     import sys
     src = open(HEADER).read()
-    depth = int(re.search(r"depth (\d+), \d+ nodes", src).group(1))
+    m = re.search(r"depth (\d+), \d+ nodes; leaf (\d+), paper-weight ([0-9.]+)", src)
     out = tmp_path / "tree.h"
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "train_selector.py"), *DATA, "--depth", str(depth),
-                        "--no-cv", "--header", str(out)], capture_output=True, text=True, cwd=ROOT)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "train_selector.py"), *DATA, "--depth", m.group(1),
+                        "--leaf", m.group(2), "--paper-weight", m.group(3), "--no-cv", "--header", str(out)],
+                       capture_output=True, text=True, cwd=ROOT)
     assert r.returncode == 0, r.stderr
     strip = lambda s: "\n".join(l for l in s.splitlines() if not l.startswith("//"))  # noqa: E731
     assert strip(out.read_text()) == strip(src)

@@ -20,6 +20,15 @@ import math
 
 import numpy as np
 
+try:  # the paper's layer tuples (optional: only for --paper-weight)
+    import os as _os
+    import sys as _sys
+    _sys.path.insert(0, _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__))))
+    from paper_1904_04174_b200 import layers as _L
+    PAPER_LAYERS = _L.RESNET50_SETS + [v for v, _ in _L.VGG16_LAYERS]
+except Exception:  # pragma: no cover
+    PAPER_LAYERS = []
+
 FEATURES = ["log2_M", "log2_F", "log2_C", "log2_K2C", "window", "stride", "valid", "log2_N", "log2_HoWo",
             "tf32", "log2_pair_tiles", "log2_flops", "intensity"]
 
@@ -64,6 +73,8 @@ def main():
     ap.add_argument("--header", default="")
     ap.add_argument("--report", default="")
     ap.add_argument("--leaf", type=int, default=2, help="min samples per leaf")
+    ap.add_argument("--paper-weight", type=float, default=10.0,
+                    help="sample-weight factor for the paper's 35 layer tuples (b1/32/256, both maths)")
     ap.add_argument("--depth", type=int, default=0, help="fixed tree depth (skips the depth search)")
     ap.add_argument("--no-cv", action="store_true", help="fit only (no cross-validation; with --depth)")
     args = ap.parse_args()
@@ -92,6 +103,10 @@ def main():
     # shapes count more; "total" regret = sum of chosen times / sum of fastest times
     tbest = np.array([min(r["times_us"].values()) for r in rows])
     wts = tbest / tbest.mean()
+    if args.paper_weight != 1.0:  # the paper's layer tuples (the workload the library is benchmarked on) count more
+        paper = {tuple(sorted(dict(l.params(b), math=m_).items())) for l in PAPER_LAYERS for b in (1, 32, 256)
+                 for m_ in (0, 1)}
+        wts = wts * np.array([args.paper_weight if tuple(sorted(r["params"].items())) in paper else 1.0 for r in rows])
     kf = KFold(5, shuffle=True, random_state=0)
     cv = {}
     for depth in ((args.depth,) if args.depth else (4, 6, 8, 10, 12, 16)):
@@ -131,7 +146,8 @@ def main():
                    "winograd_f4x4_3x3": 6}
         lines = ["// selector_tree.h -- GENERATED by tools/train_selector.py (do not edit): the learned algorithm",
                  "// selector (SURVEY.md §8(f) N4; PAPER.md:284-288), a CART tree over selector_features() in api.cpp.",
-                 f"// {len(rows)} measured shapes ({', '.join(args.data)}); depth {depth}, {t.node_count} nodes;",
+                 f"// {len(rows)} measured shapes ({', '.join(args.data)}); depth {depth}, {t.node_count} nodes; "
+                 f"leaf {args.leaf}, paper-weight {args.paper_weight:g};",
                  f"// 5-fold CV regret (chosen time / fastest time): total {cv[depth]['total']:.4f}, "
                  f"mean {cv[depth]['mean']:.4f}, median {cv[depth]['median']:.4f}, p90 {cv[depth]['p90']:.4f}.",
                  "#pragma once", "", "namespace conv2d {", "namespace selector {", "",
