@@ -20,7 +20,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "paper_1904_04174_b200", "csrc", "selector_tree.h")
 DATA = [os.path.join(ROOT, "profiles", "data", f)
-        for f in ("selector_data_r1.json", "selector_data_r1b.json", "selector_data_r1c.json")]
+        for f in ("selector_data_r1.json", "selector_data_r1b.json", "selector_data_r1c.json", "selector_data_r1d.json.gz")]
 
 
 @pytest.fixture(scope="module")
@@ -112,8 +112,11 @@ def test_predictions_are_runnable(C):
 
 def test_replayed_regret_on_measured_shapes(C):
     chosen, fastest, base = [], [], []
+    import gzip
     for path in DATA:
-        for r in json.load(open(path))["rows"]:
+        with (gzip.open(path, "rt") if path.endswith(".gz") else open(path)) as fh:
+            data = json.load(fh)
+        for r in data["rows"]:
             t = r["times_us"]
             a, v = C.conv2d_predict(C.Params(**r["params"]))
             name = C.ALGO_NAMES[a] + (f"/{v}" if a in (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1) else "")
