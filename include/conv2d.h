@@ -27,8 +27,9 @@
  * (a cudaStream_t; NULL = legacy default stream).  Parameter errors are
  * returned synchronously before anything is launched.  Kernel launch errors
  * are returned as CONV2D_ERR_CUDA (detail in conv2d_last_error()).  Results
- * are bitwise reproducible for a fixed (params, algo, device): no atomics,
- * split-K partial sums are reduced in a fixed order.
+ * are bitwise reproducible for a fixed (params, algo, tuned variant -- see
+ * conv2d_get_variant -- , device): no atomics, split-K partial sums are reduced
+ * in a fixed order.
  *
  * Thread safety: every function may be called concurrently from several host
  * threads; the auto-selector cache is mutex-protected.
