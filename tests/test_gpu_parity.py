@@ -295,6 +295,24 @@ def test_auto_hybrid_policy_times_top_candidates(cuda_ok):
     check_close(p, y.cpu().numpy(), ref, den, c.ALGO_AUTO, "auto hybrid")
 
 
+def test_pdl_chain_bitwise(cuda_ok):
+    """Programmatic dependent launch keeps stream order: a 9-conv chain (each conv reads the previous output;
+    dense, im2col, Winograd F2/F4, direct, tiled, strided paths) captured in one CUDA graph gives bit-identical
+    outputs with PDL on every launch (CONV2D_PDL=1) and on none (CONV2D_PDL=0).  A kernel that touched global
+    memory before griddepcontrol.wait would read a stale or half-written input here."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for mode in ("0", "1"):
+        env = dict(os.environ, CONV2D_PDL=mode)
+        r = subprocess.run([sys.executable, os.path.join(root, "tests", "pdl_chain.py"), root], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        out[mode] = r.stdout.split()
+    assert len(out["0"]) == 9 and out["0"] == out["1"]
+
+
 def test_device_synth_matches_host_generator(cuda_ok):
     import torch
     c = C()
