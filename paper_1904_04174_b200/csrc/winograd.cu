@@ -20,6 +20,7 @@
 // workspace (the GEMMs run on the tensor cores); the fused form is DESIGN.md "Next".
 // TF32 mode rounds U and V to TF32 with cvt.rna (reading R16); FP32 mode runs the GEMMs
 // in 3xTF32.
+#include <algorithm>
 #include <cstdlib>
 
 #include "gemm2sm.h"
@@ -359,7 +360,11 @@ cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const flo
   auto ko = mt == 2 ? (vout ? wino_output_kernel<2, true> : wino_output_kernel<2, false>)
                     : (vout ? wino_output_kernel<4, true> : wino_output_kernel<4, false>);
   const int nfx = (int)(w.cpad / 32), nfy = (int)((w.fpad + 7) / 8);
-  cudaError_t e = launch_k(kp, dim3((unsigned)(nfx * nfy) + grid_for(w.T * w.cpad / nvin)), dim3(256), 0, s, filt, p.C,
+  // 128-thread blocks: the 128-register input transform fits 4 per SM instead of 2 x 256 (same warps, half the
+  // tail granularity; measured R10 / R24 +1-1.5%).  The filter tiles loop over their 256 (c, f) items.
+  static const int pt = getenv("CONV2D_WINO_PREP_THREADS") ? atoi(getenv("CONV2D_WINO_PREP_THREADS")) : 128;
+  const int64_t in_blocks = std::min<int64_t>((w.T * w.cpad / nvin + pt - 1) / pt, 148LL * 32 * 256 / pt);
+  cudaError_t e = launch_k(kp, dim3((unsigned)(nfx * nfy + in_blocks)), dim3(pt), 0, s, filt, p.C,
                            p.F, w.cpad, w.fpad, ut_hi, ut_lo, w.three_x ? 0 : 1, nfx, nfy, in, p.H, p.W, w.TH, w.TW,
                            p.pad_top, p.pad_left, w.T, V);
   if (e != cudaSuccess) return e;
@@ -384,7 +389,11 @@ cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const flo
   g.block_n = w.block_n;
   e = launch_gemm2(p, g, s);
   if (e != cudaSuccess) return e;
-  return launch_k(ko, dim3(grid_for(w.T * p.F / (vout ? 4 : 1))), dim3(256), 0, s, Mw, w.T, w.ldm, p.F, p.HO, p.WO, w.TH, w.TW, out);
+  // 128-thread blocks here too (measured R10 / R17 +2-3% over 256)
+  static const int ot = getenv("CONV2D_WINO_OUT_THREADS") ? atoi(getenv("CONV2D_WINO_OUT_THREADS")) : 128;
+  const int64_t out_blocks = std::min<int64_t>((w.T * p.F / (vout ? 4 : 1) + ot - 1) / ot, 148LL * 32 * 256 / ot);
+  return launch_k(ko, dim3((unsigned)std::max<int64_t>(out_blocks, 1)), dim3(ot), 0, s, Mw, w.T, w.ldm, p.F, p.HO,
+                  p.WO, w.TH, w.TW, out);
 }
 
 }  // namespace conv2d
