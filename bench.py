@@ -65,6 +65,93 @@ def layer_bytes(l, batch):
     return 4 * (touched + l.window * l.window * l.channels * l.features + batch * ho * wo * l.features)
 
 
+def own_flops(l, batch, algo, C):
+    """The method's own work for one conv: Winograd F(m x m, 3x3) executes
+    2 * alpha^2 * T * C * F multiply-adds-as-flops in its batched GEMM (alpha = m + 2, T = N*ceil(Ho/m)*ceil(Wo/m));
+    every other algorithm executes the direct 2*N*Ho*Wo*K^2*C*F."""
+    ho = -(-l.rows // l.stride)
+    wo = -(-l.cols // l.stride)
+    if algo in (C.ALGO_WINOGRAD_F2X2_3X3, C.ALGO_WINOGRAD_F4X4_3X3):
+        m = 2 if algo == C.ALGO_WINOGRAD_F2X2_3X3 else 4
+        t = batch * (-(-ho // m)) * (-(-wo // m))
+        return 2 * (m + 2) ** 2 * t * l.channels * l.features
+    return l.flops(batch)
+
+
+def gemm_kernel_durations(C, convs, ws, flush, tensor_algos, reps=1):
+    """Per conv, the mean device duration (ms) of its GEMM-core launch over `reps` replays of the step graph
+    with the kernels' %globaltimer stamps on (include/conv2d_debug.h); None for CUDA-core convs.  A launch's
+    span = first CTA entry .. last CTA exit, its start clipped to the previous launch's end (PDL overlap)."""
+    import torch
+    n_gemm = sum(1 for cv in convs if cv["algo"] in tensor_algos)
+    if n_gemm == 0:
+        return None
+    reps = max(1, min(reps, 256 // n_gemm))
+    C.conv2d_debug_trace(1)
+    try:
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        with torch.cuda.graph(g, stream=cap, capture_error_mode="thread_local"):
+            cs = torch.cuda.current_stream()
+            for _ in range(reps):
+                for cv in convs:
+                    C.conv2d_forward(cv["p"], C.ALGO_AUTO, cv["x"], cv["w"], cv["y"], ws, ws.numel(), cs)
+    finally:
+        C.conv2d_debug_trace(0)
+    flush.zero_()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    t = C.conv2d_debug_trace(-1, read=True)
+    rec = 148 * 8
+    sums = [0.0] * len(convs)
+    k, prev_end = 0, None
+    for _ in range(reps):
+        for i, cv in enumerate(convs):
+            if cv["algo"] not in tensor_algos:
+                continue
+            r = t[k * rec:(k + 1) * rec]
+            k += 1
+            ent = [r[j * 8] for j in range(148) if r[j * 8]]
+            ext = [r[j * 8 + 7] for j in range(148) if r[j * 8 + 7]]
+            if not ent or not ext:
+                continue
+            start, end = min(ent), max(ext)
+            if prev_end is not None and start < prev_end:
+                start = prev_end
+            sums[i] += (end - start) / 1e6
+            prev_end = end
+    return [s / reps if cv["algo"] in tensor_algos else None for s, cv in zip(sums, convs)]
+
+
+def load_traffic(args, math_fp32_or_tf32):
+    """ncu DRAM traffic of one timed step at this workload (profiles/<round>_step_traffic*.json, written by
+    tools/step_traffic.py from the committed launch list): per GEMM-core launch and for the whole step
+    (every launch: transforms, filter prep, reduces included)."""
+    out = {"traffic": None}
+    if args.math != "fp32":
+        return out
+    for rnd in ("round2", "round1"):
+        tname = f"{rnd}_step_traffic.json" if args.global_batch == 256 else f"{rnd}_step_traffic_b{args.global_batch}.json"
+        tpath = os.path.join(ROOT, "profiles", tname)
+        if not os.path.exists(tpath):
+            continue
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        if not tj.get("gemm_launches") or tj.get("global_batch", 256) != args.global_batch:
+            continue
+        out["traffic"] = round(tj["gemm_dram_bytes"] / tj["gemm_launches"] / 1e6, 2)
+        out["traffic_unit"] = (f"MB per GEMM-core launch, ncu dram__bytes_read.sum+write.sum over one timed step "
+                               f"(profiles/{tname}, {tj['gemm_launches']} launches)")
+        if "step_dram_bytes" in tj:
+            out["traffic_step_gb"] = round(tj["step_dram_bytes"] / 1e9, 3)
+            out["traffic_step_note"] = "every launch of the step (transforms, filter prep, reduces included)"
+        if "gemm_time_share" in tj:
+            out["ncu_gemm_share_of_step"] = round(tj["gemm_time_share"], 4)
+        break
+    return out
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -180,6 +267,50 @@ def reference_arm(args):
     return 0
 
 
+def self_launch(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: re-exec this command under torch.distributed.run with
+    N local ranks (one process per GPU; rendezvous on 127.0.0.1) and return its exit status."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def plumbing_arm(args):
+    """The multi-rank launch path without a GPU (gloo): the same shard ranges, choice broadcast and
+    max-over-ranks timing as the real run; rank 0 prints one JSON line with value null."""
+    import torch
+    import torch.distributed as dist
+    from paper_1904_04174_b200.shard import broadcast_choices, max_over_ranks, shard_range
+    rank, world, _ = env_rank()
+    if world > 1:
+        dist.init_process_group("gloo")
+    d = dist if world > 1 else None
+    img0, img1 = shard_range(args.global_batch, world, rank)
+    names = sorted({l.name for _, l in L.resnet50_v15_stack()})
+    chosen = broadcast_choices({nm: (3 + rank, rank) for nm in names}, d, "cpu")
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    x = torch.arange((img1 - img0) * 1000, dtype=torch.float64).sum().item()  # stand-in work, no conv
+    t_ms = max_over_ranks((time.perf_counter() - t0) * 1e3, d, "cpu")
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": round(t_ms, 6), "plumbing": True,
+                          "config": workload_config(args, img1 - img0),
+                          "comm": {"backend": "gloo", "world_size": world},
+                          "choices_from_rank0": all(v == (3, 0) for v in chosen.values()), "checksum": x}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def workload_config(args, per_gpu):
     gb = getattr(args, "global_batch", GLOBAL_BATCH)
     return {"workload": "resnet50_v1.5_conv_stack (53 convs, BASELINE configs[4])", "global_batch": gb,
@@ -209,9 +340,12 @@ def step_trace(args, C, convs, ws, flush):
     torch.cuda.synchronize()
     t = C.conv2d_debug_trace(-1, read=True)
     rec = 148 * 8
-    out, t0, prev_end = [], None, None
+    out, t0, prev_end, k = [], None, None, 0
     for i, cv in enumerate(convs):
-        r = t[i * rec:(i + 1) * rec]
+        if cv["algo"] in (C.ALGO_DIRECT, C.ALGO_TILED):  # no GEMM-core launch, no record
+            continue
+        r = t[k * rec:(k + 1) * rec]
+        k += 1
         ctas = [r[j * 8:(j + 1) * 8] for j in range(148) if r[j * 8] != 0]
         if not ctas:
             continue
@@ -253,7 +387,21 @@ def main():
     ap.add_argument("--load-selection", default="", help="seed the selector from this table instead of tuning")
     ap.add_argument("--trace-out", default="", help="diagnostics: per-launch GEMM timeline of one extra "
                     "(untimed) graph replay of the step, JSON (include/conv2d_debug.h)")
+    ap.add_argument("--verify", action="store_true",
+                    help="N>1: gather per-conv output digests of every shard to rank 0 (NCCL) and check them "
+                         "bitwise against rank 0 recomputing that shard's images with the same kernels (P11)")
+    ap.add_argument("--plumbing", action="store_true",
+                    help="CPU-only check of the multi-rank launch path (gloo): shard ranges, choice broadcast, "
+                         "max-over-ranks timing; no convolution runs and no value is reported")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args.gpus)  # one process per GPU, as the driver's torchrun launch does
+    if int(os.environ.get("WORLD_SIZE", 1)) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE', 1)} ranks were "
+              f"launched", file=sys.stderr)
+        return 2
+    if args.plumbing:
+        return plumbing_arm(args)
     if args.impl == "reference":
         return reference_arm(args)
 
@@ -262,8 +410,6 @@ def main():
     from paper_1904_04174_b200 import conv2d as C
 
     rank, world, local = env_rank()
-    if world != args.gpus:
-        args.gpus = world if world > 1 else args.gpus
     if world > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -445,49 +591,49 @@ def main():
     tf32_peak = peaks["bf16_tflops"] / 2.0             # nominal TF32 : BF16 = 1 : 2 (B200_PROFILING.md)
     useful_peak = tf32_peak / 3.0 if math == C.MATH_FP32 else tf32_peak  # 3 MMAs per product in 3xTF32
     hbm = peaks["hbm_gbs"]
-    # dominant kernel = the tcgen05 GEMM core (gemm2sm_kernel), which runs every conv whose chosen
-    # algorithm is implicit_gemm / matmul_1x1 / winograd; its per-conv time (CUDA events on the
-    # launching stream, inside the timed region) includes the small filter-prep / split-reduce launches.
+    # Own-work accounting: a Winograd conv is credited with the multiplies it
+    # executes, 2*alpha^2*T*C*F for its batched tensor-core GEMM, not the direct-convolution flops the
+    # metric `value` uses (reading R8).  Every other conv's own work is its direct flops.
+    for cv in convs:
+        cv["own_flops"] = own_flops(cv["layer"], B, cv["algo"], C)
     tensor_algos = (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1, C.ALGO_WINOGRAD_F2X2_3X3, C.ALGO_WINOGRAD_F4X4_3X3)
-    grp = [(cv, ms) for cv, ms in zip(convs, per_conv_ms) if cv["algo"] in tensor_algos]
-    if not grp:  # degenerate: everything picked a CUDA-core algorithm
-        grp = list(zip(convs, per_conv_ms))
-    # the group's time inside the timed region = the timed step time x the group's share of the
-    # instrumented per-conv time (share = 1 when every conv runs on the GEMM core)
-    share = sum(ms for _, ms in grp) / sum(per_conv_ms)
-    g_ms = (t_ms / args.steps) * share
-    g_flops = sum(cv["flops"] for cv, _ in grp)
-    g_bytes = sum(cv["bytes"] for cv, _ in grp)
-    ach = g_flops / (g_ms / 1e3) / 1e12
-    traffic, traffic_src = None, None
-    # ncu traffic of the same workload only (tools/step_traffic.py records the batch it was captured at)
-    tname = "round1_step_traffic.json" if args.global_batch == 256 else f"round1_step_traffic_b{args.global_batch}.json"
-    tpath = os.path.join(ROOT, "profiles", tname)
-    if os.path.exists(tpath) and world == 1 and math == C.MATH_FP32:
-        with open(tpath) as fh:
-            tj = json.load(fh)
-        if tj.get("gemm_launches") and tj.get("global_batch", 256) == args.global_batch:
-            traffic = round(tj["gemm_dram_bytes"] / tj["gemm_launches"] / 1e6, 2)
-            traffic_src = (f"MB per GEMM-core launch (gemm2sm / halo), ncu dram__bytes_read.sum+write.sum over one "
-                           f"timed step ({tj['gemm_launches']} launches; profiles/round1_ncu.md)")
-    n_wino = sum(1 for cv, _ in grp if cv["algo"] in (C.ALGO_WINOGRAD_F2X2_3X3, C.ALGO_WINOGRAD_F4X4_3X3))
-    roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(useful_peak, 1), "unit": "TFLOP/s",
-            "frac": round(ach / useful_peak, 4), "traffic": traffic,
-            "traffic_unit": traffic_src, "algorithmic_mb_per_launch": round(g_bytes / len(grp) / 1e6, 2),
-            "kernel": f"GEMM core (persistent 2-CTA tcgen05 kernels gemm2sm / halo) via conv2d_forward[implicit_gemm|"
-                      f"matmul_1x1|winograd]: {len(grp)} of {len(convs)} convs, {100 * share:.1f}% of step",
-            "timing": "CUDA events at the timed steps' boundaries (launching stream) x the group's share of "
-                      "per-conv event times from K instrumented replays after the timed region",
-            "flop_accounting": f"direct-convolution flops 2*N*Ho*Wo*K^2*C*F for every conv (DESIGN.md reading R8, the "
-                               f"paper's Fig.-1 methodology); {n_wino} of {len(grp)} convs run Winograd, which executes "
-                               f"2.25x (F2x2) / 4x (F4x4) fewer multiplies, so the group's direct-normalised rate is "
-                               f"not a pure tensor-pipe utilisation",
-            "peak_source": f"{peak_src} bf16 burst {peaks['bf16_tflops']} TF/s /2 (TF32)"
-                           + (" /3 (3xTF32 useful flops)" if math == C.MATH_FP32 else "")}
-    # whole-step roofline: sum over convs of max(flops/peak, bytes/hbm)
-    roof_ms = sum(max(cv["flops"] / (useful_peak * 1e12), cv["bytes"] / (hbm * 1e9)) * 1e3 for cv in convs)
+    # dominant kernel = the tcgen05 GEMM core (gemm2sm_kernel / halo_kernel): one launch per conv whose
+    # algorithm is implicit_gemm / matmul_1x1 / winograd.  Its per-launch device durations come from the
+    # kernels' own %globaltimer stamps (include/conv2d_debug.h) in instrumented replays of the same step
+    # graph right after the timed region (L2 flushed before each); the step time is the CUDA-event time.
+    kd = gemm_kernel_durations(C, convs, ws, flush, tensor_algos, reps=min(args.steps, 4)) if rank == 0 else None
+    step_ms = t_ms / args.steps
+    grp = [cv for cv in convs if cv["algo"] in tensor_algos]
+    roof = {"bound": "tensor", "unit": "TFLOP/s", "peak": round(useful_peak, 1)}
+    if kd and grp:
+        k_ms = sum(kd[i] for i, cv in enumerate(convs) if cv["algo"] in tensor_algos)
+        k_flops = sum(cv["own_flops"] for cv in grp)
+        ach = k_flops / (k_ms / 1e3) / 1e12
+        roof.update({"achieved": round(ach, 2), "frac": round(ach / useful_peak, 4),
+                     "kernel": f"GEMM core (persistent 2-CTA tcgen05 gemm2sm_kernel / halo_kernel), {len(grp)} launches "
+                               f"per step ({len(grp)} of {len(convs)} convs), {100 * k_ms / step_ms:.1f}% of the step",
+                     "kernel_ms_per_step": round(k_ms, 3), "kernel_share_of_step": round(k_ms / step_ms, 4),
+                     "timing": "per-launch device durations (first CTA entry to last CTA exit, %globaltimer) of the "
+                               "GEMM-core launches in min(K,4) instrumented replays of the step graph after the timed "
+                               "region, L2 flushed; step time = CUDA events on the launching stream"})
+    else:
+        k_flops = sum(cv["own_flops"] for cv in convs)
+        ach = k_flops / (step_ms / 1e3) / 1e12
+        roof.update({"achieved": round(ach, 2), "frac": round(ach / useful_peak, 4),
+                     "kernel": "whole step (no GEMM-core launch timeline available on this rank)"})
+    roof["flop_accounting"] = ("own work: batched-GEMM multiplies 2*alpha^2*T*C*F for Winograd convs "
+                               "(alpha^2 = 16 / 36; transforms not counted as flops), direct flops 2*N*Ho*Wo*K^2*C*F "
+                               "for the rest; `value` stays direct-normalised (reading R8)")
+    roof["peak_source"] = (f"{peak_src} bf16 burst {peaks['bf16_tflops']} TF/s /2 (TF32)"
+                           + (" /3 (3xTF32 useful flops)" if math == C.MATH_FP32 else ""))
+    traffic = load_traffic(args, math)
+    roof.update(traffic)
+    # whole-step roofline: sum over convs of max(own flops / peak, algorithmic bytes / HBM)
+    roof_ms = sum(max(cv["own_flops"] / (useful_peak * 1e12), cv["bytes"] / (hbm * 1e9)) * 1e3 for cv in convs)
     roof["step_roofline_ms"] = round(roof_ms, 3)
-    roof["step_frac"] = round(roof_ms / (t_ms / args.steps), 4)
+    roof["step_frac"] = round(roof_ms / step_ms, 4)
+    roof["step_achieved_own_tflops"] = round(sum(cv["own_flops"] for cv in convs) / (step_ms / 1e3) / 1e12, 2)
+    roof["algorithmic_gb_per_step"] = round(sum(cv["bytes"] for cv in convs) / 1e9, 3)
 
     layers_table = []
     seen = {}
@@ -499,16 +645,17 @@ def main():
         seen[nm] = {"layer": nm, "tuple": [cv["layer"].window, cv["layer"].stride, cv["layer"].rows,
                                            cv["layer"].cols, cv["layer"].channels, cv["layer"].features],
                     "batch": B, "algo": C.ALGO_NAMES[cv["algo"]], "ms": [ms], "flops": cv["flops"],
-                    "bytes": cv["bytes"]}
+                    "own_flops": cv["own_flops"], "bytes": cv["bytes"]}
         layers_table.append(seen[nm])
     for r in layers_table:
         t = statistics.mean(r["ms"])
         r["us"] = round(1e3 * t, 2)
         r["gflops"] = round(r["flops"] / (t / 1e3) / 1e9, 1)
+        r["own_tflops"] = round(r["own_flops"] / (t / 1e3) / 1e12, 2)
         r["gbs"] = round(r["bytes"] / (t / 1e3) / 1e9, 1)
-        rl = max(r["flops"] / (useful_peak * 1e12), r["bytes"] / (hbm * 1e9)) * 1e3
+        rl = max(r["own_flops"] / (useful_peak * 1e12), r["bytes"] / (hbm * 1e9)) * 1e3
         r["roofline_frac"] = round(rl / t, 3)
-        r["bound"] = "tensor" if r["flops"] / (useful_peak * 1e12) >= r["bytes"] / (hbm * 1e9) else "hbm"
+        r["bound"] = "tensor" if r["own_flops"] / (useful_peak * 1e12) >= r["bytes"] / (hbm * 1e9) else "hbm"
         r["count"] = len(r["ms"])
         del r["ms"]
 
@@ -526,6 +673,10 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline()
 
+    verify = None
+    if args.verify:
+        verify = verify_shards(args, C, convs, ws, stream, world, rank, dev)
+
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 1), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(t_ms / args.steps, 3), "higher_is_better": True,
@@ -535,7 +686,10 @@ def main():
                                selection_s=round(tune_s, 2)),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "wall_s_timed": round(wall, 3),
-                "pct_of_peak": round(100 * value / 1e3 / (useful_peak * world), 2)}
+                "pct_of_peak": round(100 * roof["step_achieved_own_tflops"] / useful_peak, 2),
+                "comm": {"backend": dist.get_backend() if world > 1 else None, "world_size": world}}
+        if verify is not None:
+            line["verify"] = verify
         if args.layers_out:
             with open(args.layers_out, "w") as f:
                 json.dump({"bench": line, "layers": layers_table}, f, indent=1)
@@ -543,6 +697,51 @@ def main():
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def output_digests(convs):
+    """Per conv: two exact integer digests of the output's bit patterns (plain and position-weighted
+    int64 sums; integer addition is associative, so the digest itself is deterministic)."""
+    import torch
+    rows = []
+    for cv in convs:
+        bits = cv["y"].view(torch.int32).long()
+        wgt = torch.arange(bits.numel(), device=bits.device, dtype=torch.int64) % 1021 + 1
+        rows.append(torch.stack([bits.sum(), (bits * wgt).sum()]))
+    return torch.stack(rows)
+
+
+def verify_shards(args, C, convs, ws, stream, world, rank, dev):
+    """P11 across ranks (--verify, off the timed path): every rank's output digests are all-gathered to
+    rank 0 (NCCL), which regenerates each other rank's images from their global indices, runs the same
+    kernels (rank 0's broadcast choices; same per-GPU batch, so the same launch plan) and requires
+    bit-identical digests."""
+    import torch
+    import torch.distributed as dist
+    from paper_1904_04174_b200.shard import shard_range
+    mine = output_digests(convs)
+    if world == 1:
+        return {"ranks_checked": 0, "note": "single rank: nothing to cross-check"}
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    ok, checked = True, 0
+    if rank == 0:
+        for r in range(1, world):
+            img0, _ = shard_range(args.global_batch, world, r)
+            for cv in convs:
+                l = cv["layer"]
+                per_img = l.rows * l.cols * l.channels
+                C.conv2d_synth_fill(cv["x"], cv["x"].numel(), synth.stream_key(synth.SEED, cv["id"], synth.ROLE_INPUT),
+                                    img0 * per_img, 0)
+            for cv in convs:
+                C.conv2d_forward(cv["p"], C.ALGO_AUTO, cv["x"], cv["w"], cv["y"], ws, ws.numel(), stream)
+            torch.cuda.synchronize()
+            ok = ok and bool(torch.equal(output_digests(convs), parts[r]))
+            checked += 1
+    flag = torch.tensor([int(ok)], dtype=torch.int32, device=dev)
+    dist.broadcast(flag, 0)
+    return {"ranks_checked": checked, "bitwise": bool(flag.item()), "digest": "int64 sums of output bits per conv",
+            "how": "NCCL all_gather of shard digests; rank 0 recomputes each shard's images with the same kernels"}
 
 
 def run_e2e(args, C, convs, ws, stream, world, dev):

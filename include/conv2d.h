@@ -185,7 +185,10 @@ conv2d_status_t conv2d_save_selection(const char* path);
 conv2d_status_t conv2d_load_selection(const char* path, int* loaded);
 
 /* Last per-algorithm best times (microseconds) from the most recent autotune on
- * this thread; times[a] < 0 for algorithms not timed.  times must hold CONV2D_NUM_ALGOS. */
+ * this thread; times[a] < 0 for algorithms not timed.  times must hold CONV2D_NUM_ALGOS.
+ * A candidate whose launch is refused during tuning (e.g. a grid-limit error) is dropped
+ * with a warning on stderr and reports < 0; a fault that leaves the stream
+ * unusable is returned as CONV2D_ERR_CUDA instead. */
 void conv2d_last_tune_times(double times_us[CONV2D_NUM_ALGOS]);
 
 /* Number of kernel launches conv2d_forward(p, algo) issues (AUTO: of the cached choice,

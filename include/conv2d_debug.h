@@ -5,6 +5,8 @@
 #ifndef CONV2D_B200_DEBUG_H
 #define CONV2D_B200_DEBUG_H
 
+#include "conv2d.h"
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -22,6 +24,15 @@ extern "C" {
  * that count; returns 0 if nothing was copied and -1 on a CUDA error.  Costs one predicated
  * branch per stamp site when disabled.  Not thread-safe; for tools/ and bench diagnostics. */
 int conv2d_debug_trace(int enable, unsigned long long* host, int n);
+
+/* K-split of the launch plan conv2d_forward(p, algo) would run now (with the variant currently recorded
+ * for p): *splits = 1 (no split: every output is one accumulation over the whole K = KH*KW*C in a fixed
+ * order), s > 1 (every tile's K range is cut into s parts, summed in fixed order by a reduce kernel), or
+ * -s (remainder split: only the partial last wave's tiles are cut s ways).  Two plans with equal
+ * *splits = 1 give bitwise identical outputs for the same image (the P11 shard check);
+ * a split count depends on the tile count and so on the batch.  Status as conv2d_supports, plus
+ * CONV2D_ERR_UNSUPPORTED when algo cannot run p.  Host-only, no device work. */
+conv2d_status_t conv2d_debug_splits(const conv2d_params_t* p, conv2d_algo_t algo, int* splits);
 
 #ifdef __cplusplus
 }

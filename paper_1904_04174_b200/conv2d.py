@@ -40,7 +40,7 @@ EXPORTED = ["conv2d_output_shape", "conv2d_flop_count", "conv2d_supports", "conv
             "conv2d_forward", "conv2d_autotune", "conv2d_selected", "conv2d_set_selected",
             "conv2d_clear_selection_cache", "conv2d_last_tune_times", "conv2d_launch_count",
             "conv2d_synth_fill", "conv2d_status_string", "conv2d_algo_name", "conv2d_last_error",
-            "conv2d_debug_trace", "conv2d_save_selection", "conv2d_load_selection",
+            "conv2d_debug_trace", "conv2d_debug_splits", "conv2d_save_selection", "conv2d_load_selection",
             "pool2d_output_shape", "pool2d_forward", "conv2d_set_autotune_flush", "conv2d_get_variant",
             "conv2d_set_variant", "conv2d_predict", "conv2d_set_auto_policy"]
 
@@ -84,6 +84,7 @@ _lib.conv2d_algo_name.argtypes = [ctypes.c_int]
 _lib.conv2d_algo_name.restype = ctypes.c_char_p
 _lib.conv2d_last_error.argtypes = []
 _lib.conv2d_debug_trace.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+_lib.conv2d_debug_splits.argtypes = [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
 _lib.conv2d_save_selection.argtypes = [ctypes.c_char_p]
 _lib.conv2d_set_autotune_flush.argtypes = [_vp, ctypes.c_size_t]
 _lib.conv2d_load_selection.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int)]
@@ -245,6 +246,20 @@ def conv2d_set_variant(p: Params, algo: int, variant: int) -> None:
     _check(_lib.conv2d_set_variant(ctypes.byref(p.c()), int(algo), int(variant)), "conv2d_set_variant")
 
 
+def conv2d_variants(p: Params, algo: int) -> list:
+    """The parameter variants the auto-selector enumerates for (p, algo): exactly those conv2d_set_variant
+    accepts (probes 0..31, restores the recorded variant)."""
+    if algo not in (ALGO_IMPLICIT_GEMM, ALGO_MATMUL_1X1):
+        return [0]
+    keep = conv2d_get_variant(p, algo)
+    out = []
+    for v in range(32):
+        if _lib.conv2d_set_variant(ctypes.byref(p.c()), int(algo), v) == OK:
+            out.append(v)
+    conv2d_set_variant(p, algo, keep)
+    return out
+
+
 AUTO_MEASURE, AUTO_PREDICT, AUTO_HYBRID = 0, 1, 2
 
 
@@ -321,6 +336,13 @@ def conv2d_debug_trace(enable: int, read: bool = False) -> list:
     return list(buf[:got]) if read else []
 
 
+def conv2d_debug_splits(p: Params, algo: int) -> int:
+    """include/conv2d_debug.h: K-split of the plan conv2d_forward(p, algo) would run now (1 = none)."""
+    v = ctypes.c_int()
+    _check(_lib.conv2d_debug_splits(ctypes.byref(p.c()), int(algo), ctypes.byref(v)), "conv2d_debug_splits")
+    return int(v.value)
+
+
 # ------------------------------------------------------------------ convenience (torch in, torch out)
 def params_for(x, w, stride=(1, 1), padding: int = PAD_SAME, math: int = MATH_FP32) -> Params:
     n, h, wd, c = x.shape
@@ -338,11 +360,22 @@ def forward(x, w, stride=(1, 1), padding: int = PAD_SAME, algo: int = ALGO_AUTO,
     (n, ho, wo, f), _ = conv2d_output_shape(p)
     if not (x.is_cuda and w.is_cuda and x.dtype == torch.float32 and w.dtype == torch.float32):
         raise ValueError("x and w must be float32 CUDA tensors")
+    if w.device != x.device:
+        raise ValueError(f"x is on {x.device} but w is on {w.device}")
+    if out is not None:  # the kernels write n*ho*wo*f dense floats from out's base pointer
+        if (tuple(out.shape) != (n, ho, wo, f) or out.dtype != torch.float32 or not out.is_contiguous()
+                or out.device != x.device):
+            raise ValueError(f"out must be a contiguous float32 tensor of shape {(n, ho, wo, f)} on {x.device}; "
+                             f"got {tuple(out.shape)} {out.dtype} on {out.device} (contiguous={out.is_contiguous()})")
+    if workspace is not None and workspace.device != x.device:
+        raise ValueError(f"workspace is on {workspace.device}, not {x.device}")
     x = x.contiguous()
     w = w.contiguous()
-    y = out if out is not None else torch.empty((n, ho, wo, f), dtype=torch.float32, device=x.device)
-    need = conv2d_query_workspace(p, algo)
-    if workspace is None or workspace.numel() < need:
-        workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device) if need else None
-    conv2d_forward(p, algo, x, w, y, workspace, need if workspace is not None else 0, stream)
+    with torch.cuda.device(x.device):  # launch on x's GPU, on that device's current stream by default
+        y = out if out is not None else torch.empty((n, ho, wo, f), dtype=torch.float32, device=x.device)
+        need = conv2d_query_workspace(p, algo)
+        if workspace is None or workspace.numel() * workspace.element_size() < need:
+            workspace = torch.empty(max(need, 16), dtype=torch.uint8, device=x.device) if need else None
+        conv2d_forward(p, algo, x, w, y, workspace, need if workspace is not None else 0,
+                       stream if stream is not None else torch.cuda.current_stream(x.device))
     return y

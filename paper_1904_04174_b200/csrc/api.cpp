@@ -105,7 +105,9 @@ bool algo_supports(const Problem& q, conv2d_algo_t a) {
       const int CC = q.C < 8 ? q.C : 8;
       const size_t xs = (size_t)(7 * q.SH + q.KH) * (15 * q.SW + q.KW) * (CC + 1);
       const size_t smem = sizeof(float) * ((xs + 3) / 4 * 4 + (size_t)q.KH * q.KW * CC * 64);
-      return smem <= 227 * 1024;
+      // 1-D grid of (WO/16) x (HO/8) x N x (F/64) CTAs must fit gridDim.x
+      const int64_t blocks = (int64_t)((q.WO + 15) / 16) * ((q.HO + 7) / 8) * q.N * ((q.F + 63) / 64);
+      return smem <= 227 * 1024 && blocks <= 0x7FFFFFFFLL;
     }
     case CONV2D_ALGO_MATMUL_1X1:
       return q.KH == 1 && q.KW == 1 && q.SH == 1 && q.SW == 1;
@@ -220,6 +222,7 @@ conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int de
     flush_bytes = g_flush_bytes;
   }
   for (int i = 0; i < CONV2D_NUM_ALGOS; ++i) g_tune_times[i] = -1.0;
+  bool failed_any = false;
   cudaEvent_t e0, e1;
   cudaError_t ce = cudaEventCreate(&e0);
   if (ce != cudaSuccess) return cuda_fail(ce, "cudaEventCreate");
@@ -255,7 +258,21 @@ conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int de
       const int v = masks[vi];
       if (!measured(ai, v)) continue;
       if (gemm_like) igemm_set_variant(q, is_1x1, v);
-      for (int w = 0; w < warm && st == CONV2D_OK; ++w) st = run_algo(q, a, in, filt, out, ws, s);
+      st = run_algo(q, a, in, filt, out, ws, s);
+      if (st == CONV2D_ERR_CUDA) {
+        // a measurement failure drops that candidate and logs a warning.  Only a launch that
+        // was refused (non-sticky: the stream still synchronises cleanly) is skipped; a fault that
+        // poisoned the context is returned to the caller.
+        const std::string why = g_last_error;
+        cudaGetLastError();
+        if (cudaStreamSynchronize(s) != cudaSuccess) break;
+        fprintf(stderr, "[conv2d] autotune: %s variant %d failed to launch (%s); candidate dropped\n",
+                conv2d_algo_name(a), v, why.c_str());
+        failed_any = true;
+        st = CONV2D_OK;
+        continue;
+      }
+      for (int w = 1; w < warm && st == CONV2D_OK; ++w) st = run_algo(q, a, in, filt, out, ws, s);
       for (int r = 0; r < reps && st == CONV2D_OK; ++r) {
         if (flush) {  // cache-cold repetition: evict L2 outside the timed events
           ce = cudaMemsetAsync(flush, r & 0xFF, flush_bytes, s);
@@ -292,6 +309,8 @@ conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int de
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (st != CONV2D_OK) return st;
+  if (best == CONV2D_ALGO_AUTO)
+    return fail(CONV2D_ERR_CUDA, failed_any ? "autotune: every candidate failed to launch" : "autotune: no candidate");
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     g_cache[key_of(p, dev)] = best;
@@ -901,6 +920,23 @@ conv2d_status_t pool2d_forward(const pool2d_params_t* p, const float* in, float*
 
 int conv2d_debug_trace(int enable, unsigned long long* host, int n) {
   return conv2d::gemm2_trace(enable, host, n);
+}
+
+conv2d_status_t conv2d_debug_splits(const conv2d_params_t* p, conv2d_algo_t algo, int* splits) {
+  if (!splits) return fail(CONV2D_ERR_NULL, "splits is NULL");
+  Problem q;
+  std::string why;
+  if (!shape_of(p, &q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
+  if (!valid_algo(algo) || algo == CONV2D_ALGO_AUTO) return fail(CONV2D_ERR_INVALID_PARAMS, "need a concrete algorithm");
+  if (!algo_supports(q, algo)) return fail(CONV2D_ERR_UNSUPPORTED, "algorithm does not support these params");
+  switch (algo) {
+    case CONV2D_ALGO_IMPLICIT_GEMM: *splits = igemm_split_desc(q, false); break;
+    case CONV2D_ALGO_MATMUL_1X1: *splits = igemm_split_desc(q, true); break;
+    case CONV2D_ALGO_WINOGRAD_F2X2_3X3: *splits = winograd_splits(q, 2); break;
+    case CONV2D_ALGO_WINOGRAD_F4X4_3X3: *splits = winograd_splits(q, 4); break;
+    default: *splits = 1;
+  }
+  return CONV2D_OK;
 }
 
 }  // extern "C"

@@ -210,6 +210,14 @@ int igemm_launches(const Problem& p, bool is_1x1) {
   return (pl.b_mn ? 1 : 2) + (pl.pad ? 1 : 0) + (pl.splits > 1 || pl.rsplit ? 1 : 0);
 }
 
+int igemm_split_desc(const Problem& p, bool is_1x1) {
+  const Plan pl = make_plan(p, is_1x1, variant_of(p, is_1x1));
+  if (pl.a_mode == A_S2D) return 1;
+  return pl.rsplit ? -gemm2_rsplit_factor(((p.M() + 255) / 256) * ((p.F + pl.block_n - 1) / pl.block_n),
+                                          (int)(pl.kpad / 32))
+                   : pl.splits;
+}
+
 cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const float* filt, float* out, void* ws,
                          cudaStream_t s) {
   const Plan pl = make_plan(p, is_1x1, variant_of(p, is_1x1));

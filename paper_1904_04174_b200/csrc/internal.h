@@ -41,11 +41,15 @@ int igemm_variants(const Problem& p, bool is_1x1, int* masks);  // tunable param
 void igemm_set_variant(const Problem& p, bool is_1x1, int v);
 bool igemm_get_variant(const Problem& p, bool is_1x1, int* v);  // false if never set
 int igemm_launches(const Problem& p, bool is_1x1);
+// K-split of the plan conv2d_forward would run now: 1 = none, s > 1 = every tile split s ways,
+// -s = remainder split (the partial last wave's tiles split s ways)
+int igemm_split_desc(const Problem& p, bool is_1x1);
 cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const float* filt, float* out, void* ws,
                          cudaStream_t s);
 // ---- winograd.cu
 size_t winograd_workspace(const Problem& p, int mt);  // mt = output tile: 2 (F2x2) or 4 (F4x4)
 int winograd_launches(const Problem& p, int mt);
+int winograd_splits(const Problem& p, int mt);  // K-split count of the batched GEMMs (1 = none)
 cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const float* filt, float* out, void* ws,
                             cudaStream_t s);
 // ---- synth.cu

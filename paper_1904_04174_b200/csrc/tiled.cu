@@ -23,7 +23,8 @@ constexpr int NTHREADS = (TW / PX) * TH * (FB / FV);  // 256
 __global__ void __launch_bounds__(NTHREADS) tiled_kernel(const float* __restrict__ in,
                                                          const float* __restrict__ filt, float* __restrict__ out,
                                                          int H, int W, int C, int F, int KH, int KW, int SH, int SW,
-                                                         int HO, int WO, int PT, int PL, int fblocks) {
+                                                         int HO, int WO, int PT, int PL, int fblocks, int wtiles,
+                                                         int htiles) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ float smem[];
@@ -34,9 +35,14 @@ __global__ void __launch_bounds__(NTHREADS) tiled_kernel(const float* __restrict
   float* xs = smem;                                  // [IH][IW][CCP]
   float* ws = smem + ((IH * IW * CCP + 3) & ~3);     // [KH][KW][CC][FB], 16-byte aligned for LDS.128
 
-  const int n = blockIdx.z / fblocks;
-  const int fb0 = (blockIdx.z % fblocks) * FB;
-  const int ho0 = blockIdx.y * TH, wo0 = blockIdx.x * TW;
+  // 1-D grid (gridDim.z <= 65535 would cap N * fblocks): x = ((n * fblocks + fb) * htiles + ht) * wtiles + wt
+  const int64_t bid = blockIdx.x;
+  const int wt = (int)(bid % wtiles);
+  const int ht = (int)((bid / wtiles) % htiles);
+  const int64_t nf = bid / ((int64_t)wtiles * htiles);
+  const int n = (int)(nf / fblocks);
+  const int fb0 = (int)(nf % fblocks) * FB;
+  const int ho0 = ht * TH, wo0 = wt * TW;
   const int ih0 = ho0 * SH - PT, iw0 = wo0 * SW - PL;
 
   const int t = threadIdx.x;
@@ -122,9 +128,11 @@ cudaError_t launch_tiled(const Problem& p, const float* in, const float* filt, f
     if (e != cudaSuccess) return e;
   }
   const int fblocks = (p.F + FB - 1) / FB;
-  dim3 grid((p.WO + TW - 1) / TW, (p.HO + TH - 1) / TH, (unsigned)(p.N * fblocks));
-  return launch_k(tiled_kernel, grid, dim3(NTHREADS), smem, s, in, filt, out, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH,
-                  p.SW, p.HO, p.WO, p.pad_top, p.pad_left, fblocks);
+  const int wtiles = (p.WO + TW - 1) / TW, htiles = (p.HO + TH - 1) / TH;
+  const int64_t blocks = (int64_t)wtiles * htiles * p.N * fblocks;
+  if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;  // tiled_grid_ok() rejects this in supports()
+  return launch_k(tiled_kernel, dim3((unsigned)blocks), dim3(NTHREADS), smem, s, in, filt, out, p.H, p.W, p.C, p.F,
+                  p.KH, p.KW, p.SH, p.SW, p.HO, p.WO, p.pad_top, p.pad_left, fblocks, wtiles, htiles);
 }
 
 }  // namespace conv2d

@@ -332,6 +332,7 @@ unsigned grid_for(int64_t total) {
 
 size_t winograd_workspace(const Problem& p, int mt) { return make_wplan(p, mt).total; }
 int winograd_launches(const Problem& p, int mt) { return 3 + (make_wplan(p, mt).splits > 1 ? 1 : 0); }
+int winograd_splits(const Problem& p, int mt) { return make_wplan(p, mt).splits; }
 
 cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const float* filt, float* out, void* ws,
                             cudaStream_t s) {

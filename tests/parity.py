@@ -5,6 +5,9 @@ Inputs for both come from paper_1904_04174_b200.synth only.
 """
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 
 import oracle as O
@@ -64,10 +67,20 @@ def supported_algos(p):
     return [a for a in range(1, c.NUM_ALGOS) if c.conv2d_supports(p, a)]
 
 
+def record_err(what: str, algo: int, math: int, e: float, n: int = 0):
+    """CONV2D_ERRLOG=path: append one JSON line per parity check (error census behind the P10 ceilings)."""
+    path = os.environ.get("CONV2D_ERRLOG")
+    if path:
+        with open(path, "a") as fh:
+            fh.write(json.dumps({"what": what, "algo": C().ALGO_NAMES[algo], "math": int(math), "err": float(e),
+                                 "n": int(n)}) + "\n")
+
+
 def check_close(p, y: np.ndarray, y_ref: np.ndarray, denom: np.ndarray, algo: int, what: str = ""):
     assert y.shape == y_ref.shape, (what, y.shape, y_ref.shape)
     assert np.all(np.isfinite(y)), f"{what}: non-finite output (unwritten or NaN)"
     e = O.normalized_error(y, y_ref, denom)
+    record_err(what, algo, p.math, e, y.size)
     tol = tol_for(algo, p.math)
     assert e <= tol, f"{what}: normalized error {e:.3e} > {tol:.0e}"
     return e

@@ -158,18 +158,36 @@ def test_edge_cases(cuda_ok, case):
 
 def test_determinism_and_shard_bitwise(cuda_ok):
     """P11: fixed (params, algo) -> bitwise identical reruns; batch slices run separately give
-    the same bits as the full batch when the launch configuration is the same."""
+    the same bits as the full batch when neither launch plan splits K (conv2d_debug_splits == 1), for
+    every algorithm; with a K split on either side (the split count follows the batch's tile count)
+    the slices are held to the tolerance instead."""
+    c = C()
     p = P(4, 28, 28, 64, 64, 3, 3)
     x, w = make_inputs(p, layer_id=500)
     for a in supported_algos(p):
         y1 = gpu_conv(p, x, w, a)
         y2 = gpu_conv(p, x, w, a)
-        assert np.array_equal(y1, y2), C().conv2d_algo_name(a)
-    ph = p.replace(batch=2)
-    for a in (C().ALGO_DIRECT, C().ALGO_TILED):
-        full = gpu_conv(p, x, w, a)
-        for r in range(2):
-            assert np.array_equal(gpu_conv(ph, x[2 * r:2 * r + 2], w, a), full[2 * r:2 * r + 2])
+        assert np.array_equal(y1, y2), c.conv2d_algo_name(a)
+    bitwise = set()
+    for case in [(8, 80, 80, 64, 64, 3, 3), (8, 80, 80, 64, 128, 1, 1), (8, 120, 120, 32, 128, 3, 3, 2, 2),
+                 (8, 40, 40, 128, 128, 3, 3), (8, 7, 7, 512, 512, 3, 3), (8, 61, 57, 3, 64, 7, 7, 2, 2)]:
+        for math in MATHS:
+            p = P(*case, math=math)
+            x, w = make_inputs(p, layer_id=501)
+            ref, den = O.conv2d(oparams(p), x, w, with_denom=True)
+            ph = p.replace(batch=4)
+            for a in supported_algos(p):
+                full = gpu_conv(p, x, w, a)
+                same_plan = c.conv2d_debug_splits(p, a) == 1 and c.conv2d_debug_splits(ph, a) == 1
+                for r in range(2):
+                    part = gpu_conv(ph, x[4 * r:4 * r + 4], w, a)
+                    if same_plan:
+                        assert np.array_equal(part, full[4 * r:4 * r + 4]), (case, math, c.conv2d_algo_name(a), r)
+                        bitwise.add(c.conv2d_algo_name(a))
+                    else:
+                        check_close(ph, part, ref[4 * r:4 * r + 4], den[4 * r:4 * r + 4], a, f"shard {case} {a}")
+    # every algorithm is covered by at least one bitwise shard comparison
+    assert bitwise >= {c.ALGO_NAMES[i] for i in range(1, c.NUM_ALGOS)}, bitwise
 
 
 def test_autotune_and_auto_forward(cuda_ok):

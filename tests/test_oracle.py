@@ -297,3 +297,17 @@ def test_normalized_error_metric():
     assert O.normalized_error(y, y, np.array([1.0, 0.0, 1.0])) == 0.0
     assert O.normalized_error(y + np.array([1e-6, 0, 0]), y, np.array([10.0, 0.0, 1.0])) == pytest.approx(1e-7)
     assert O.normalized_error(np.array([0.0, 1e-30]), np.array([0.0, 0.0]), np.array([1.0, 0.0])) == float("inf")
+
+
+def test_golden_config1_regenerates_from_its_generator():
+    """The committed P6 fixture is what tools/gen_golden_config1.py derives (torch float64 + pure-Python brute
+    force, neither touching oracle/ nor the CUDA path)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "gen_golden_config1", os.path.join(os.path.dirname(GOLD), "..", "tools", "gen_golden_config1.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    fresh = gen.generate()
+    committed = _gold("config1_integer.json")
+    for key in ("same_s1", "valid_s1", "same_s2"):
+        assert fresh[key] == committed[key], key

@@ -36,8 +36,10 @@ def main():
             n += 1
             us += t
             byts += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)
-    json.dump({"source": path, "global_batch": batch, "gemm_launches": n, "gemm_us": us, "gemm_dram_bytes": byts, "total_us": total},
-              sys.stdout, indent=1)
+    step_bytes = sum(m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0) for m in per.values())
+    json.dump({"source": path, "global_batch": batch, "gemm_launches": n, "gemm_us": us, "gemm_dram_bytes": byts,
+               "total_us": total, "gemm_time_share": us / total if total else None, "step_launches": len(per),
+               "step_dram_bytes": step_bytes}, sys.stdout, indent=1)
     print()
 
 
