@@ -21,7 +21,7 @@ import oracle as O
 from paper_1904_04174_b200 import layers as L
 from paper_1904_04174_b200 import synth
 
-from .parity import C, TOL_FP32, TOL_TF32, record_err, tol_for
+from .parity import C, TOL_FP32, TOL_TF32, ceiling_for, record_err, tol_for
 
 pytestmark = pytest.mark.gpu
 MATHS = (0, 1)
@@ -113,7 +113,7 @@ def _check_every_algo(case, what):
             assert bool(torch.isfinite(y).all()), f"{what} {c.ALGO_NAMES[a]} math={math}: unwritten/non-finite"
             e = float(np.max(np.abs(_gather(y, shape, idx) - ref) / den))
             record_err(f"{what} math={math}", a, math, e, len(idx))
-            tol = tol_for(a, math)
+            tol = min(tol_for(a, math), ceiling_for(a, math))
             assert e <= tol, f"{what} {c.ALGO_NAMES[a]} math={math}: err {e:.3e} > {tol}"
             errs[(c.ALGO_NAMES[a], math)] = e
     return errs
@@ -145,7 +145,7 @@ def test_stack_b256_tf32_auto(cuda_ok, layer_id, layer):
     ref, den = _oracle_points(case, p, idx)
     e = float(np.max(np.abs(_gather(y, shape, idx) - ref) / den))
     record_err(f"{layer.name} b256 auto", algo, 1, e, len(idx))
-    assert e <= TOL_TF32, f"{layer.name} b256 tf32 auto={c.ALGO_NAMES[algo]}: err {e:.3e}"
+    assert e <= min(TOL_TF32, ceiling_for(algo, 1)), f"{layer.name} b256 tf32 auto={c.ALGO_NAMES[algo]}: err {e:.3e}"
 
 
 @pytest.mark.parametrize("layer_id,layer", STACK, ids=[l.name for _, l in STACK])
