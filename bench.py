@@ -242,6 +242,96 @@ def cpu_baseline(target_s: float = 15.0):
                       f" full oracle incl. double accumulation; {flops/1e9:.2f} GFLOP in {t:.2f} s"}
 
 
+def config1_leg(args):
+    """BASELINE.json configs[0] (N=1, 8x8x4 -> 8x8x8, 3x3, stride 1, SAME): per algorithm the
+    GPU time of one conv2d_forward -- the median of single CUDA-graph replays bracketed by events, and the
+    per-call time of 1000 back-to-back replays -- next to the oracle's time on this host (cpu_baseline leg:
+    1 thread and every core).  Prints one JSON line (not the bench contract line)."""
+    import torch
+    import oracle as O
+    from paper_1904_04174_b200 import conv2d as C
+    O.build()
+    torch.cuda.set_device(0)
+    p0 = C.Params(1, 8, 8, 4, 8, 3, 3, 1, 1, C.PAD_SAME)
+    xh = synth.input_nhwc(1, 8, 8, 4, layer_id=1)
+    wh = synth.filter_hwcf(3, 3, 4, 8, layer_id=1)
+    x, w = torch.from_numpy(xh).cuda(), torch.from_numpy(wh).cuda()
+    y = torch.empty(512, device="cuda")
+    flops = C.conv2d_flop_count(p0)
+    gpu = {}
+    for math in (C.MATH_FP32, C.MATH_TF32):
+        p = p0.replace(math=math)
+        for a in range(1, C.NUM_ALGOS):
+            if not C.conv2d_supports(p, a):
+                continue
+            need = C.conv2d_query_workspace(p, a)
+            ws = torch.empty(max(need, 16), dtype=torch.uint8, device="cuda")
+            for _ in range(5):
+                C.conv2d_forward(p, a, x, w, y, ws, ws.numel())
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                C.conv2d_forward(p, a, x, w, y, ws, ws.numel(), torch.cuda.current_stream())
+            g1000 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g1000, capture_error_mode="thread_local"):
+                for _ in range(1000):
+                    C.conv2d_forward(p, a, x, w, y, ws, ws.numel(), torch.cuda.current_stream())
+            g.replay()
+            g1000.replay()
+            torch.cuda.synchronize()
+            singles = []
+            for _ in range(50):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                g.replay()
+                e1.record()
+                e1.synchronize()
+                singles.append(e0.elapsed_time(e1) * 1e3)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g1000.replay()
+            e1.record()
+            e1.synchronize()
+            per_call = e0.elapsed_time(e1)  # ms for 1000 calls = us per call
+            gpu[f"{C.ALGO_NAMES[a]}/{'tf32' if math else 'fp32'}"] = {
+                "single_us": round(statistics.median(singles), 2), "back_to_back_us": round(per_call, 3),
+                "launches": C.conv2d_launch_count(p, a), "gflops_back_to_back": round(flops / (per_call * 1e3), 2)}
+    op = O.Params(1, 8, 8, 4, 8, 3, 3, 1, 1, O.SAME)
+    cores = os.cpu_count() or 1
+    orc = {}
+    for th in (1, cores):
+        ts = []
+        for _ in range(200):
+            t0 = time.perf_counter()
+            O.conv2d(op, xh, wh, threads=th)
+            ts.append((time.perf_counter() - t0) * 1e6)
+        orc[f"threads_{th}"] = {"median_us": round(statistics.median(ts), 2), "min_us": round(min(ts), 2)}
+    print(json.dumps({"config1": {"workload": "BASELINE configs[0]: N=1, 8x8x4, 3x3, F=8, stride 1, SAME",
+                                  "flops": flops, "gpu": gpu, "oracle": orc, "cores": cores,
+                                  "oracle_note": "oracle/ through ctypes (includes the call overhead), "
+                                                 "median of 200 calls"}}), flush=True)
+    return 0
+
+
+def oracle_layers_leg(args):
+    """cpu_baseline leg, per layer (the Fig.-1 tables' oracle column): the oracle's GFLOP/s on one image of
+    every ResNet-50 set and VGG-16 layer, all host cores; one JSON line."""
+    import oracle as O
+    O.build()
+    cores = os.cpu_count() or 1
+    out = {}
+    for l in list(L.RESNET50_SETS) + [l for l, _ in L.VGG16_LAYERS]:
+        x = synth.input_nhwc(1, l.rows, l.cols, l.channels, layer_id=5000)
+        w = synth.filter_hwcf(l.window, l.window, l.channels, l.features, layer_id=5000)
+        op = O.Params(1, l.rows, l.cols, l.channels, l.features, l.window, l.window, l.stride, l.stride, O.SAME)
+        t0 = time.perf_counter()
+        O.conv2d(op, x, w, threads=cores)
+        t = time.perf_counter() - t0
+        out[l.name] = {"gflops": round(l.flops(1) / t / 1e9, 2), "ms": round(t * 1e3, 2)}
+    print(json.dumps({"oracle_layers": out, "cores": cores, "sample": "1 image per layer"}), flush=True)
+    return 0
+
+
 def reference_arm(args):
     rank, world, _ = env_rank()
     if rank != 0:
@@ -393,6 +483,10 @@ def main():
     ap.add_argument("--plumbing", action="store_true",
                     help="CPU-only check of the multi-rank launch path (gloo): shard ranges, choice broadcast, "
                          "max-over-ranks timing; no convolution runs and no value is reported")
+    ap.add_argument("--config1", action="store_true",
+                    help="BASELINE configs[0]: GPU us per algorithm + the oracle's us (1 thread, all cores)")
+    ap.add_argument("--oracle-layers", action="store_true",
+                    help="cpu_baseline leg per layer: the oracle's GFLOP/s on one image of every paper layer")
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         return self_launch(args.gpus)  # one process per GPU, as the driver's torchrun launch does
@@ -402,6 +496,10 @@ def main():
         return 2
     if args.plumbing:
         return plumbing_arm(args)
+    if args.config1:
+        return config1_leg(args)
+    if args.oracle_layers:
+        return oracle_layers_leg(args)
     if args.impl == "reference":
         return reference_arm(args)
 

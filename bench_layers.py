@@ -27,6 +27,8 @@ from paper_1904_04174_b200 import layers as L  # noqa: E402
 from paper_1904_04174_b200 import synth  # noqa: E402
 from bench import layer_bytes, load_peaks  # noqa: E402
 
+FFMA_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4 TF/s: the CUDA-core fp32 FMA ceiling at max SM clock
+
 
 def layer_set(name):
     if name == "resnet50":
@@ -127,10 +129,17 @@ def main():
             ent = {"best_us": round(best * 1e3, 2), "median_us": round(med * 1e3, 2),
                    "gflops": round(flops / (best / 1e3) / 1e9, 1), "gbs": round(nbytes / (best / 1e3) / 1e9, 1),
                    "roofline_frac": round(roof_ms / best, 3)}
+            if a in (C.ALGO_DIRECT, C.ALGO_TILED):
+                # CUDA-core kernels graded against their own ceiling: the FFMA pipe (148 SMs x 128 FMA/clk x
+                # 2 flop x 1.965 GHz = 74.4 TF/s) or HBM, whichever bounds the layer
+                ffma_ms = max(flops / (FFMA_TFLOPS * 1e12), nbytes / (hbm * 1e9)) * 1e3
+                ent["ffma_frac"] = round(ffma_ms / best, 3)
             if a == C.ALGO_AUTO:
                 ent["chose"] = C.ALGO_NAMES[C.conv2d_selected(p)]
             row["algos"][name] = ent
         rows.append(row)
+        if not row["algos"]:
+            continue
         cand = [k for k in row["algos"] if k != "auto"] or list(row["algos"])
         best_algo = min(cand, key=lambda k: row["algos"][k]["best_us"])
         print(f"{l.name:4s} {str(row['tuple']):26s} roof {row['roofline_us']:9.1f}us  " +

@@ -101,14 +101,8 @@ bool algo_supports(const Problem& q, conv2d_algo_t a) {
     case CONV2D_ALGO_DIRECT:
     case CONV2D_ALGO_IMPLICIT_GEMM:
       return true;
-    case CONV2D_ALGO_TILED: {
-      const int CC = q.C < 8 ? q.C : 8;
-      const size_t xs = (size_t)(7 * q.SH + q.KH) * (15 * q.SW + q.KW) * (CC + 1);
-      const size_t smem = sizeof(float) * ((xs + 3) / 4 * 4 + (size_t)q.KH * q.KW * CC * 64);
-      // 1-D grid of (WO/16) x (HO/8) x N x (F/64) CTAs must fit gridDim.x
-      const int64_t blocks = (int64_t)((q.WO + 15) / 16) * ((q.HO + 7) / 8) * q.N * ((q.F + 63) / 64);
-      return smem <= 227 * 1024 && blocks <= 0x7FFFFFFFLL;
-    }
+    case CONV2D_ALGO_TILED:
+      return tiled_supported(q);
     case CONV2D_ALGO_MATMUL_1X1:
       return q.KH == 1 && q.KW == 1 && q.SH == 1 && q.SW == 1;
     case CONV2D_ALGO_WINOGRAD_F2X2_3X3:

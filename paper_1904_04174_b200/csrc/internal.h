@@ -35,6 +35,7 @@ cudaError_t launch_pool(const PoolProblem& p, const float* x, float* y, cudaStre
 cudaError_t launch_direct(const Problem& p, const float* in, const float* filt, float* out, cudaStream_t s);
 // ---- tiled.cu
 cudaError_t launch_tiled(const Problem& p, const float* in, const float* filt, float* out, cudaStream_t s);
+bool tiled_supported(const Problem& p);  // the tile's shared-memory chunk fits and the 1-D grid fits gridDim.x
 // ---- igemm.cu (implicit GEMM and 1x1 matmul on tcgen05)
 size_t igemm_workspace(const Problem& p, bool is_1x1);  // max over variants
 int igemm_variants(const Problem& p, bool is_1x1, int* masks);  // tunable parameter masks (<= 8)

@@ -1,41 +1,87 @@
 // tiled.cu -- CONV2D_ALGO_TILED: tiled direct convolution on CUDA cores
 // ("tiled algorithm", SPEC.md:210-230 tile_rows x tile_cols x
-// feature_block).  B200 design:
-//   * CTA = one image x (TH=8) x (TW=16) output tile x (FB=64) features, 256 threads.
-//   * Per channel chunk (CC <= 8), the input halo tile ((TH-1)S+KH) x ((TW-1)S+KW) x CC
-//     and the filter chunk KH x KW x CC x FB are staged in shared memory (coalesced
-//     global loads, zero-filled padding), so each input element is read from L2 once
-//     per CTA instead of once per tap.
-//   * Each thread keeps a 4-pixel x 8-feature register tile (32 fp32 accumulators):
-//     per (c, kh, kw) it does 2 LDS.128 (filter) + 4 LDS (input) for 32 FFMA.
-//   * Input rows are padded to CC+1 floats to break the 4-way bank conflict between
-//     the four pixel groups of a warp.
-// Exact fp32 FFMA, (c-chunk, c, kh, kw) accumulation order.
+// feature_block).  B200 design (round 2):
+//   * CTA = 128 threads = 4 warps (three CTAs per SM) over one image x (TH x TW) output tile x FB features.  A warp owns a
+//     (32/CG) x (CG*4) pixel block and 16 features; lane (r, g) computes 4 consecutive output pixels of row
+//     r x 16 features (64 fp32 accumulators, 32 packed FFMA2 per input value pair).  WFG = FB/16 warps share
+//     a pixel block (the others stack vertically), so a warp's filter reads are shared-memory broadcasts.
+//   * Per channel chunk (CC <= 16) the input halo ((TH-1)S+KH) x ((TW-1)S+KW) is staged channel-major
+//     xs[c][row][col] (NHWC float4 global loads of 4 channels where C % 4 == 0; zero padding) and the filter
+//     chunk ws[kh][kw][c][FB] (float4 loads); each thread then reads its input row segment for (c, kh)
+//     once into registers -- (4-1)*S+KW floats, 16-byte LDS -- and reuses it for every kw (templated on the
+//     common (KW, S); a generic path reads per tap).
+//   * FFMA2 (fma.rn.f32x2, sm_100): each instruction does two independent fp32 FMAs, so every output
+//     element still sees exactly one RN fp32 FMA per tap: exact-fp32 results, (c-chunk, c, kh, kw) order.
+// Bound: FFMA pipe (74.4 TF/s at 1965 MHz) when the 16-feature x 4-pixel register tile is full; input
+// and filter shared-memory reads are ~1 wavefront per 32..64 FMAs per warp.
 #include "internal.h"
 #include "launch.cuh"
 
 namespace conv2d {
 namespace {
 
-constexpr int TH = 8, TW = 16, FB = 64, PX = 4, FV = 8, CCMAX = 8;
-constexpr int NTHREADS = (TW / PX) * TH * (FB / FV);  // 256
+constexpr int NT = 128, NW = NT / 32, PX = 4, FV = 16, CCMAX = 16;
+constexpr int SMEM_BUDGET = 72 * 1024;  // three CTAs per SM (registers allow three 128-thread CTAs)
 
-__global__ void __launch_bounds__(NTHREADS) tiled_kernel(const float* __restrict__ in,
-                                                         const float* __restrict__ filt, float* __restrict__ out,
-                                                         int H, int W, int C, int F, int KH, int KW, int SH, int SW,
-                                                         int HO, int WO, int PT, int PL, int fblocks, int wtiles,
-                                                         int htiles) {
+struct TGeo {
+  int cg, wfg, th, tw, fb, cc, ih, iw, iwp;
+  size_t smem;
+  bool ok;
+};
+
+TGeo geometry(const Problem& p) {
+  TGeo g{};
+  g.cg = p.WO >= 32 ? 8 : p.WO >= 16 ? 4 : 2;
+  g.wfg = p.F > 32 ? 4 : p.F > 16 ? 2 : 1;
+  g.fb = FV * g.wfg;
+  g.th = (32 / g.cg) * (NW / g.wfg);
+  g.tw = g.cg * PX;
+  g.ih = (g.th - 1) * p.SH + p.KH;
+  g.iw = (g.tw - 1) * p.SW + p.KW;
+  g.iwp = (g.iw + 3) & ~3;
+  const size_t per_c = sizeof(float) * ((size_t)g.ih * g.iwp + (size_t)p.KH * p.KW * g.fb);
+  const int cc = (int)(SMEM_BUDGET / per_c);
+  g.cc = cc < CCMAX ? cc : CCMAX;
+  if (g.cc > p.C) g.cc = p.C;
+  if (g.cc >= 4) g.cc &= ~3;  // whole channel quads per chunk (float4 staging)
+  g.smem = per_c * (size_t)(g.cc > 0 ? g.cc : 1);
+  const int64_t blocks = (int64_t)((p.WO + g.tw - 1) / g.tw) * ((p.HO + g.th - 1) / g.th) * p.N *
+                         ((p.F + g.fb - 1) / g.fb);
+  g.ok = g.cc >= 1 && blocks <= 0x7FFFFFFFLL;
+  return g;
+}
+
+__device__ __forceinline__ void fma_tile(float2 (&acc)[PX][FV / 2], const float (&xv)[PX], const float4 (&w4)[FV / 4]) {
+#pragma unroll
+  for (int i = 0; i < PX; ++i) {
+    const float2 xx = make_float2(xv[i], xv[i]);
+#pragma unroll
+    for (int j = 0; j < FV / 4; ++j) {
+      acc[i][2 * j] = __ffma2_rn(xx, make_float2(w4[j].x, w4[j].y), acc[i][2 * j]);
+      acc[i][2 * j + 1] = __ffma2_rn(xx, make_float2(w4[j].z, w4[j].w), acc[i][2 * j + 1]);
+    }
+  }
+}
+
+// KW_, SW_ > 0: compile-time window width / stride (row segment cached in registers); 0: runtime
+template <int KW_, int SW_>
+__global__ void __launch_bounds__(NT, 3) tiled_kernel(const float* __restrict__ in, const float* __restrict__ filt,
+                                                      float* __restrict__ out, int H, int W, int C, int F, int KH,
+                                                      int KWr, int SH, int SWr, int HO, int WO, int PT, int PL,
+                                                      int cg, int wfg, int cc_max, int wtiles, int htiles,
+                                                      int fblocks) {
   pdl_trigger();
   pdl_wait();
-  extern __shared__ float smem[];
-  const int CC = C < CCMAX ? C : CCMAX;
-  const int CCP = CC + 1;
-  const int IH = (TH - 1) * SH + KH;
-  const int IW = (TW - 1) * SW + KW;
-  float* xs = smem;                                  // [IH][IW][CCP]
-  float* ws = smem + ((IH * IW * CCP + 3) & ~3);     // [KH][KW][CC][FB], 16-byte aligned for LDS.128
+  const int KW = KW_ ? KW_ : KWr;
+  const int SW = SW_ ? SW_ : SWr;
+  extern __shared__ float4 smem4[];
+  float* smem = reinterpret_cast<float*>(smem4);
+  const int FB = FV * wfg;
+  const int rows_w = 32 / cg;                 // pixel rows per warp block
+  const int TH = rows_w * (NW / wfg), TW = cg * PX;
+  const int IH = (TH - 1) * SH + KH, IW = (TW - 1) * SW + KW, IWP = (IW + 3) & ~3;
 
-  // 1-D grid (gridDim.z <= 65535 would cap N * fblocks): x = ((n * fblocks + fb) * htiles + ht) * wtiles + wt
+  // 1-D grid: x = ((n * fblocks + fb) * htiles + ht) * wtiles + wt
   const int64_t bid = blockIdx.x;
   const int wt = (int)(bid % wtiles);
   const int ht = (int)((bid / wtiles) % htiles);
@@ -45,94 +91,167 @@ __global__ void __launch_bounds__(NTHREADS) tiled_kernel(const float* __restrict
   const int ho0 = ht * TH, wo0 = wt * TW;
   const int ih0 = ho0 * SH - PT, iw0 = wo0 * SW - PL;
 
-  const int t = threadIdx.x;
-  const int fv = t % (FB / FV);
-  const int tx = (t / (FB / FV)) % (TW / PX);
-  const int ty = t / ((FB / FV) * (TW / PX));
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int fg = warp % wfg, pb = warp / wfg;
+  const int row = pb * rows_w + lane / cg;     // output row within the tile
+  const int colg = lane % cg;                  // 4-pixel column group
 
-  float acc[PX][FV];
+  float* xs = smem;                                        // [cc][IH][IWP]
+  float* ws = smem + (size_t)cc_max * IH * IWP;             // [KH*KW][cc][FB]
+
+  float2 acc[PX][FV / 2];
 #pragma unroll
   for (int i = 0; i < PX; ++i)
 #pragma unroll
-    for (int j = 0; j < FV; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < FV / 2; ++j) acc[i][j] = make_float2(0.f, 0.f);
 
   const float* xin = in + (int64_t)n * H * W * C;
-  for (int c0 = 0; c0 < C; c0 += CC) {
-    const int cc = (C - c0) < CC ? (C - c0) : CC;
+  const bool vec_c = (C & 3) == 0 && (cc_max & 3) == 0;
+  for (int c0 = 0; c0 < C; c0 += cc_max) {
+    const int cc = (C - c0) < cc_max ? (C - c0) : cc_max;
     __syncthreads();  // previous chunk fully consumed
-    // stage input halo tile (zero outside the image and beyond cc)
-    for (int e = t; e < IH * IW * CC; e += NTHREADS) {
-      const int c = e % CC;
-      const int col = (e / CC) % IW;
-      const int row = e / (CC * IW);
-      const int ih = ih0 + row, iw = iw0 + col;
-      float v = 0.f;
-      if (c < cc && ih >= 0 && ih < H && iw >= 0 && iw < W) v = __ldg(xin + ((int64_t)ih * W + iw) * C + c0 + c);
-      xs[(row * IW + col) * CCP + c] = v;
+    if (vec_c) {  // 4 channels per float4 load; cc is a multiple of 4 (host rounds cc_max; C % 4 == 0)
+      const int cq = cc >> 2;
+      for (int e = t; e < IH * IW * cq; e += NT) {
+        const int q = e % cq;
+        const int pix = e / cq;
+        const int col = pix % IW, r = pix / IW;
+        const int ih = ih0 + r, iw = iw0 + col;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ih >= 0 && ih < H && iw >= 0 && iw < W)
+          v = __ldg(reinterpret_cast<const float4*>(xin + ((int64_t)ih * W + iw) * C + c0) + q);
+        float* d = xs + ((size_t)(4 * q) * IH + r) * IWP + col;
+        d[0] = v.x;
+        d[(size_t)IH * IWP] = v.y;
+        d[(size_t)2 * IH * IWP] = v.z;
+        d[(size_t)3 * IH * IWP] = v.w;
+      }
+    } else {
+      for (int e = t; e < IH * IW * cc; e += NT) {
+        const int c = e % cc;
+        const int pix = e / cc;
+        const int col = pix % IW, r = pix / IW;
+        const int ih = ih0 + r, iw = iw0 + col;
+        float v = 0.f;
+        if (ih >= 0 && ih < H && iw >= 0 && iw < W) v = __ldg(xin + ((int64_t)ih * W + iw) * C + c0 + c);
+        xs[((size_t)c * IH + r) * IWP + col] = v;
+      }
     }
-    // stage filter chunk
-    for (int e = t; e < KH * KW * CC * FB; e += NTHREADS) {
-      const int f = e % FB;
-      const int c = (e / FB) % CC;
-      const int khw = e / (FB * CC);
-      float v = 0.f;
-      if (c < cc && fb0 + f < F) v = __ldg(filt + ((int64_t)khw * C + c0 + c) * F + fb0 + f);
-      ws[e] = v;
+    // filter chunk: ws[(tap * cc_max + c) * FB + f], features fastest (float4 where F % 4 == 0)
+    if ((F & 3) == 0) {
+      const int fq = FB >> 2;
+      for (int e = t; e < KH * KW * cc * fq; e += NT) {
+        const int q = e % fq;
+        const int c = (e / fq) % cc;
+        const int tap = e / (fq * cc);
+        const int f = fb0 + 4 * q;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (f < F) v = __ldg(reinterpret_cast<const float4*>(filt + ((int64_t)tap * C + c0 + c) * F + f));
+        *reinterpret_cast<float4*>(ws + ((size_t)tap * cc_max + c) * FB + 4 * q) = v;
+      }
+    } else {
+      for (int e = t; e < KH * KW * cc * FB; e += NT) {
+        const int fl = e % FB;
+        const int c = (e / FB) % cc;
+        const int tap = e / (FB * cc);
+        const int f = fb0 + fl;
+        ws[((size_t)tap * cc_max + c) * FB + fl] = (f < F) ? __ldg(filt + ((int64_t)tap * C + c0 + c) * F + f) : 0.f;
+      }
     }
     __syncthreads();
     for (int c = 0; c < cc; ++c) {
       for (int kh = 0; kh < KH; ++kh) {
-        const float* xrow = xs + ((ty * SH + kh) * IW) * CCP + c;
-        for (int kw = 0; kw < KW; ++kw) {
-          const float4* wp = reinterpret_cast<const float4*>(ws + ((kh * KW + kw) * CC + c) * FB + fv * FV);
-          const float4 wa = wp[0], wb = wp[1];
-          const float wv[FV] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+        const float* xr = xs + ((size_t)c * IH + row * SH + kh) * IWP + colg * PX * SW;
+        const float* wr = ws + ((size_t)(kh * KW) * cc_max + c) * FB + fg * FV;
+        if constexpr (KW_ > 0) {
+          constexpr int L = (PX - 1) * SW_ + KW_;
+          constexpr int L4 = L / 4;
+          float seg[L4 * 4 + 4];
 #pragma unroll
-          for (int i = 0; i < PX; ++i) {
-            const float xv = xrow[((tx * PX + i) * SW + kw) * CCP];
+          for (int q = 0; q < L4; ++q) {
+            const float4 v = *reinterpret_cast<const float4*>(xr + 4 * q);
+            seg[4 * q] = v.x;
+            seg[4 * q + 1] = v.y;
+            seg[4 * q + 2] = v.z;
+            seg[4 * q + 3] = v.w;
+          }
 #pragma unroll
-            for (int j = 0; j < FV; ++j) acc[i][j] = fmaf(xv, wv[j], acc[i][j]);
+          for (int q = L4 * 4; q < L; ++q) seg[q] = xr[q];
+#pragma unroll
+          for (int kw = 0; kw < KW_; ++kw) {
+            float4 w4[FV / 4];
+            const float4* wp = reinterpret_cast<const float4*>(wr + (size_t)kw * cc_max * FB);
+#pragma unroll
+            for (int j = 0; j < FV / 4; ++j) w4[j] = wp[j];
+            float xv[PX];
+#pragma unroll
+            for (int i = 0; i < PX; ++i) xv[i] = seg[i * SW_ + kw];
+            fma_tile(acc, xv, w4);
+          }
+        } else {
+          for (int kw = 0; kw < KW; ++kw) {
+            float4 w4[FV / 4];
+            const float4* wp = reinterpret_cast<const float4*>(wr + (size_t)kw * cc_max * FB);
+#pragma unroll
+            for (int j = 0; j < FV / 4; ++j) w4[j] = wp[j];
+            float xv[PX];
+#pragma unroll
+            for (int i = 0; i < PX; ++i) xv[i] = xr[i * SW + kw];
+            fma_tile(acc, xv, w4);
           }
         }
       }
     }
   }
-  const int ho = ho0 + ty;
+  const int ho = ho0 + row;
   if (ho >= HO) return;
+  const int f0 = fb0 + fg * FV;
 #pragma unroll
   for (int i = 0; i < PX; ++i) {
-    const int wo = wo0 + tx * PX + i;
+    const int wo = wo0 + colg * PX + i;
     if (wo >= WO) continue;
-    float* o = out + (((int64_t)n * HO + ho) * WO + wo) * F + fb0 + fv * FV;
-    const int f = fb0 + fv * FV;
-    if ((F % 4) == 0 && f + FV <= F) {
-      reinterpret_cast<float4*>(o)[0] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-      reinterpret_cast<float4*>(o)[1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    float* o = out + (((int64_t)n * HO + ho) * WO + wo) * F + f0;
+    if ((F & 3) == 0 && f0 + FV <= F) {
+#pragma unroll
+      for (int j = 0; j < FV / 4; ++j)
+        reinterpret_cast<float4*>(o)[j] = make_float4(acc[i][2 * j].x, acc[i][2 * j].y, acc[i][2 * j + 1].x,
+                                                      acc[i][2 * j + 1].y);
     } else {
 #pragma unroll
-      for (int j = 0; j < FV; ++j)
-        if (f + j < F) o[j] = acc[i][j];
+      for (int j = 0; j < FV / 2; ++j) {
+        if (f0 + 2 * j < F) o[2 * j] = acc[i][j].x;
+        if (f0 + 2 * j + 1 < F) o[2 * j + 1] = acc[i][j].y;
+      }
     }
   }
 }
 
+template <int KW_, int SW_>
+cudaError_t launch_t(const Problem& p, const TGeo& g, const float* in, const float* filt, float* out, cudaStream_t s) {
+  const cudaError_t e = smem_attr_once<tiled_kernel<KW_, SW_>>(SMEM_BUDGET);
+  if (e != cudaSuccess) return e;
+  const int fblocks = (p.F + g.fb - 1) / g.fb;
+  const int wtiles = (p.WO + g.tw - 1) / g.tw, htiles = (p.HO + g.th - 1) / g.th;
+  const int64_t blocks = (int64_t)wtiles * htiles * p.N * fblocks;
+  return launch_k(tiled_kernel<KW_, SW_>, dim3((unsigned)blocks), dim3(NT), g.smem, s, in, filt, out, p.H, p.W,
+                  p.C, p.F, p.KH, p.KW, p.SH, p.SW, p.HO, p.WO, p.pad_top, p.pad_left, g.cg, g.wfg, g.cc, wtiles,
+                  htiles, fblocks);
+}
+
 }  // namespace
 
+bool tiled_supported(const Problem& p) { return geometry(p).ok; }
+
 cudaError_t launch_tiled(const Problem& p, const float* in, const float* filt, float* out, cudaStream_t s) {
-  const int CC = p.C < CCMAX ? p.C : CCMAX;
-  const int IH = (TH - 1) * p.SH + p.KH, IW = (TW - 1) * p.SW + p.KW;
-  const size_t smem = sizeof(float) * ((((size_t)IH * IW * (CC + 1)) + 3) / 4 * 4 + (size_t)p.KH * p.KW * CC * FB);
-  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  {
-    const cudaError_t e = smem_attr_once<tiled_kernel>(227 * 1024);
-    if (e != cudaSuccess) return e;
-  }
-  const int fblocks = (p.F + FB - 1) / FB;
-  const int wtiles = (p.WO + TW - 1) / TW, htiles = (p.HO + TH - 1) / TH;
-  const int64_t blocks = (int64_t)wtiles * htiles * p.N * fblocks;
-  if (blocks > 0x7FFFFFFFLL) return cudaErrorInvalidConfiguration;  // tiled_grid_ok() rejects this in supports()
-  return launch_k(tiled_kernel, dim3((unsigned)blocks), dim3(NTHREADS), smem, s, in, filt, out, p.H, p.W, p.C, p.F,
-                  p.KH, p.KW, p.SH, p.SW, p.HO, p.WO, p.pad_top, p.pad_left, fblocks, wtiles, htiles);
+  const TGeo g = geometry(p);
+  if (!g.ok) return cudaErrorInvalidConfiguration;  // algo_supports(TILED) == tiled_supported() rejects these
+  if (p.KW == 1 && p.SW == 1) return launch_t<1, 1>(p, g, in, filt, out, s);
+  if (p.KW == 1 && p.SW == 2) return launch_t<1, 2>(p, g, in, filt, out, s);
+  if (p.KW == 3 && p.SW == 1) return launch_t<3, 1>(p, g, in, filt, out, s);
+  if (p.KW == 3 && p.SW == 2) return launch_t<3, 2>(p, g, in, filt, out, s);
+  if (p.KW == 5 && p.SW == 1) return launch_t<5, 1>(p, g, in, filt, out, s);
+  if (p.KW == 7 && p.SW == 2) return launch_t<7, 2>(p, g, in, filt, out, s);
+  return launch_t<0, 0>(p, g, in, filt, out, s);
 }
 
 }  // namespace conv2d
