@@ -83,8 +83,13 @@ struct HCfg {
   static constexpr int HALO_BYTES = Geo<GEOM>::HALO_BYTES;
   static constexpr int BHALF = (BN / 2) * BK * 4;
   static constexpr int BFULL = BN * BK * 4;
-  static constexpr int HS = THREE_X ? 2 : 3;                           // halo slots
-  static constexpr int HSLOT = HALO_BYTES * (THREE_X ? 2 : 1);         // hi (+ lo)
+  // ATM (3xTF32, G3X3): the transform warps copy every tap's A rows out of the halo into TMEM, hi and lo
+  // (a 64-column slot per tap: hi | lo), and the MMAs take A from TMEM -- shared memory then only feeds B
+  // to the tensor core (fact 12: with A_hi and the halo lo read from smem by every MMA, R4 was bound by
+  // shared-memory bandwidth at ~0.67 of the tensor peak).  The halo slots hold hi only.
+  static constexpr bool ATM = THREE_X && GEOM == G3X3;
+  static constexpr int HS = (THREE_X && !ATM) ? 2 : 3;                 // halo slots
+  static constexpr int HSLOT = HALO_BYTES * ((THREE_X && !ATM) ? 2 : 1);  // hi (+ lo)
   // CONCAT (3xTF32, BN = 64, where smem operand reads bound the MMA): B stage Z = BN rows (CTA0:
   // B_hi, CTA1: B_lo) for one N'=2BN MMA hi x [B_hi | B_lo] -- A_hi is read once for both products --
   // plus X = BN/2 rows of B_hi (this CTA's half) for lo x B_hi; the epilogue adds the two column halves.
@@ -101,8 +106,11 @@ struct HCfg {
   static constexpr int S = BRES ? Geo<GEOM>::KB_PER_UNIT : ((BUDGET / BSTAGE) > 12 ? 12 : (BUDGET / BSTAGE));
   static_assert(!BRES || S * BSTAGE <= BUDGET, "resident B does not fit");
   static constexpr int SMEM = HS * HSLOT + S * BSTAGE + EPI + RAWB + 1024 + 512;
-  static constexpr uint32_t TMEM_COLS = 2 * ACC;
+  static constexpr int AS = ATM ? (512 - 2 * ACC) / 64 : 0;            // ATM: TMEM tap slots
+  static constexpr uint32_t A_COL0 = 2 * ACC;                            // first column of the tap slots
+  static constexpr uint32_t TMEM_COLS = ATM ? 512 : 2 * ACC;
   static_assert(S >= 2, "halo kernel needs >= 2 B stages");
+  static_assert(!ATM || AS >= 2, "ATM needs >= 2 TMEM tap slots");
   static_assert(2 * ACC <= 512, "TMEM");
 };
 
@@ -148,7 +156,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   uint64_t* tmem_empty = tmem_full + 2;
   uint64_t* raw_ld = tmem_empty + 2;     // raw patch landed (TMA -> transform)
   uint64_t* raw_empty = raw_ld + 1;      // raw patch consumed (transform -> producer)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 1);
+  uint64_t* a_full = raw_empty + 1;      // ATM: tap slot written (both CTAs' transform warps -> leader MMA)
+  uint64_t* a_empty = a_full + 4;        // ATM: tap slot read by the MMAs (commit -> transform warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -161,7 +171,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     for (int h = 0; h < HS; ++h) {
       mbar_init(&h_ld[h], 1);
       mbar_init(&h_full[h], 2 * 128);
-      mbar_init(&h_empty[h], 1);
+      mbar_init(&h_empty[h], C_::ATM ? 128 : 1);  // ATM: this CTA's transform threads release the halo
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&a_full[i], 2 * 128);
+      mbar_init(&a_empty[i], 1);
     }
     for (int s = 0; s < S; ++s) {
       mbar_init(&b_full[s], 1);
@@ -259,7 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     if (rank == 0) {  // whole warp, converged: operands stay warp-uniform
       constexpr uint32_t idesc = idesc_tf32(256, BN);
       constexpr uint32_t idesc2 = idesc_tf32(256, 2 * BN);  // 3x: hi x [B_hi | B_lo]
-      uint32_t hit = 0, bit = 0, ai = 0;
+      uint32_t hit = 0, bit = 0, ai = 0, ait = 0;
       if (C_::BRES && cid < args.total) {
         mbar_wait(&b_full[0], 0);
         tc_fence_after();
@@ -272,8 +286,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const uint32_t d = tmem_base + (uint32_t)(acc * C_::ACC);
         for (int cb = 0; cb < args.ncb; ++cb, ++hit) {
           const int h = hit % HS;
-          mbar_wait(&h_full[h], (hit / HS) & 1);
-          tc_fence_after();
+          if (!C_::ATM) {
+            mbar_wait(&h_full[h], (hit / HS) & 1);
+            tc_fence_after();
+          }
           for (int kb = 0; kb < KBU; ++kb, ++bit) {
             const uint64_t soff = soff_next;
             if constexpr (GEOM == GS2D) soff_next = args.soff[kb + 1 < 8 ? kb + 1 : 7];
@@ -292,6 +308,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               return GEOM == GS2D ? umma_desc_sw64_kmajor_sbo(a, HWD * G_::ROWB)
                                   : umma_desc_sw128_kmajor_sbo(a, HWD * G_::ROWB, 0u);
             };
+            if constexpr (C_::ATM) {  // A from the TMEM tap slot the transform warps filled
+              const int slot = (int)(ait % C_::AS);
+              mbar_wait(&a_full[slot], (ait / C_::AS) & 1);
+              tc_fence_after();
+              const uint32_t ahi = tmem_base + C_::A_COL0 + (uint32_t)(slot * 64), alo = ahi + 32;
+              const uint64_t dbx = umma_desc_sw128_kmajor(smem_u32(b_x(s)));
+              const uint64_t dbz = C_::CONCAT ? umma_desc_sw128_kmajor(smem_u32(b_z(s))) : 0;
+              const uint64_t dbl = C_::CONCAT ? 0 : umma_desc_sw128_kmajor(smem_u32(b_lo(s)));
+#pragma unroll
+              for (int k = 0; k < BK / 8; ++k) {
+                const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);
+                const uint32_t accum = (cb > 0 || kb > 0 || k > 0) ? 1u : 0u;
+                if (C_::CONCAT) {
+                  mma_tf32_2sm_ts_warp(d, ahi + (uint32_t)(k * 8), dbz + adv, idesc2, accum);
+                  mma_tf32_2sm_ts_warp(d, alo + (uint32_t)(k * 8), dbx + adv, idesc, 1u);
+                } else {
+                  mma_tf32_2sm_ts_warp(d, alo + (uint32_t)(k * 8), dbx + adv, idesc, accum);
+                  mma_tf32_2sm_ts_warp(d, ahi + (uint32_t)(k * 8), dbl + adv, idesc, 1u);
+                  mma_tf32_2sm_ts_warp(d, ahi + (uint32_t)(k * 8), dbx + adv, idesc, 1u);
+                }
+              }
+              if (!C_::BRES) mma_commit_2sm_mc_warp(&b_empty[s], 0x3);
+              mma_commit_2sm_mc_warp(&a_empty[slot], 0x3);
+              ++ait;
+              continue;
+            }
             const int tap0 = GEOM == GS2D ? 0 : kb;
             const uint64_t dah0 = view(smem_u32(halo_hi(h)), tap0);
             const uint64_t dal0 = THREE_X ? view(smem_u32(halo_lo(h)), tap0) : 0;
@@ -328,7 +370,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             }
             if (!C_::BRES) mma_commit_2sm_mc_warp(&b_empty[s], 0x3);
           }
-          mma_commit_2sm_mc_warp(&h_empty[h], 0x3);
+          if (!C_::ATM) mma_commit_2sm_mc_warp(&h_empty[h], 0x3);
         }
         mma_commit_2sm_mc_warp(&tmem_full[acc], 0x3);
       }
@@ -338,10 +380,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     // ============================ halo transform (128 threads) ============================
     const int t = threadIdx.x;
     const uint32_t h_full_leader = mapa(smem_u32(h_full), 0);
-    uint32_t hit = 0;
+    const uint32_t a_full_leader = mapa(smem_u32(a_full), 0);
+    uint32_t hit = 0, ait = 0;
     for (int tt = cid; tt < args.total; tt += ncl) {
       for (int cb = 0; cb < args.ncb; ++cb, ++hit) {
         const int h = hit % HS;
+        if constexpr (C_::ATM) {
+          // thread t = A row t = output pixel (ho0 + t / 8, wo0 + t % 8); tap (r, c) reads halo pixel
+          // (t / 8 + r) * 16 + (t % 8 + c): its 32 channels (one 128-byte SWIZZLE_128B row) -> TMEM lane t,
+          // hi = raw fp32 (the MMA reads its top 19 bits) in slot columns [0, 32), lo = x - trunc_tf32(x) in [32, 64)
+          mbar_wait(&h_ld[h], (hit / HS) & 1);
+          const uint32_t hb = smem_u32(halo_hi(h));
+          const uint32_t lane_addr = tmem_base + ((uint32_t)(warp * 32) << 16) + C_::A_COL0;
+          for (int tap = 0; tap < 9; ++tap, ++ait) {
+            const int p = (t / TW + tap / 3) * HWD + (t % TW + tap % 3);
+            float hi[32], lo[32];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 v = lds128(hb + sw128_offset((uint32_t)p, (uint32_t)j));
+              hi[4 * j] = v.x;
+              hi[4 * j + 1] = v.y;
+              hi[4 * j + 2] = v.z;
+              hi[4 * j + 3] = v.w;
+              lo[4 * j] = v.x - tf32_hi(v.x);
+              lo[4 * j + 1] = v.y - tf32_hi(v.y);
+              lo[4 * j + 2] = v.z - tf32_hi(v.z);
+              lo[4 * j + 3] = v.w - tf32_hi(v.w);
+            }
+            const int slot = (int)(ait % C_::AS);
+            if (ait >= (uint32_t)C_::AS) mbar_wait(&a_empty[slot], ((ait / C_::AS) - 1) & 1);
+            tc_fence_after();
+            tmem_st32(lane_addr + (uint32_t)(slot * 64), hi);
+            tmem_st32(lane_addr + (uint32_t)(slot * 64 + 32), lo);
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive_remote(a_full_leader + (uint32_t)(slot * sizeof(uint64_t)));
+          }
+          mbar_arrive(&h_empty[h]);  // every tap of this halo is in TMEM: the producer may refill the slot
+          continue;
+        }
         if (GEOM == GS2D && args.raw) {
           // build the s2d halo: pixel p = (hi, wi) of the 19 x 16 halo, 16-byte chunk k = slots 4k..4k+3,
           // slot = (b*2 + d)*C + c <- raw[2*hi + b][2*wi + d][c]; SWIZZLE_64B placement (chunk k of the
