@@ -328,14 +328,40 @@ unsigned grid_for(int64_t total) {
   return (unsigned)(b < 1 ? 1 : b);
 }
 
+// filter transform alone (the fused F(2x2) path, wino_fused.cu): one 128-thread block per 32 (c) x 8 (f) tile
+template <int MT>
+__global__ void __launch_bounds__(128) wino_filter_kernel(const float* __restrict__ w, int C, int F, int64_t cpad,
+                                                          int64_t fpad, float* __restrict__ ut_hi,
+                                                          float* __restrict__ ut_lo, int mode, int nfx) {
+  pdl_trigger();
+  pdl_wait();
+  wino_filter_tile<MT>(w, C, F, cpad, fpad, ut_hi, ut_lo, mode, (int)blockIdx.x % nfx, (int)blockIdx.x / nfx);
+}
+
 }  // namespace
 
-size_t winograd_workspace(const Problem& p, int mt) { return make_wplan(p, mt).total; }
-int winograd_launches(const Problem& p, int mt) { return 3 + (make_wplan(p, mt).splits > 1 ? 1 : 0); }
-int winograd_splits(const Problem& p, int mt) { return make_wplan(p, mt).splits; }
+cudaError_t launch_wino_filter(int mt, const float* w, int C, int F, int64_t cpad, int64_t fpad, float* ut_hi,
+                               float* ut_lo, bool three_x, cudaStream_t s) {
+  const int nfx = (int)(cpad / 32), nfy = (int)((fpad + 7) / 8);
+  return launch_k(mt == 2 ? wino_filter_kernel<2> : wino_filter_kernel<4>, dim3((unsigned)(nfx * nfy)), dim3(128), 0,
+                  s, w, C, F, cpad, fpad, ut_hi, ut_lo, three_x ? 0 : 1, nfx);
+}
+
+size_t winograd_workspace(const Problem& p, int mt) {
+  const size_t unfused = make_wplan(p, mt).total;
+  return mt == 2 ? std::max(unfused, wino_fused_workspace(p)) : unfused;
+}
+int winograd_launches(const Problem& p, int mt) {
+  if (mt == 2 && wino_fused_ok(p)) return 2;
+  return 3 + (make_wplan(p, mt).splits > 1 ? 1 : 0);
+}
+int winograd_splits(const Problem& p, int mt) { return mt == 2 && wino_fused_ok(p) ? 1 : make_wplan(p, mt).splits; }
 
 cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const float* filt, float* out, void* ws,
                             cudaStream_t s) {
+  // F(2x2): the fused kernel (wino_fused.cu) whenever its plan applies and the pointers are TMA-aligned
+  if (mt == 2 && wino_fused_ok(p) && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0)
+    return launch_wino_fused(p, in, filt, out, ws, s);
   const WPlan w = make_wplan(p, mt);
   uint8_t* b = static_cast<uint8_t*>(ws);
   float* ut_hi = reinterpret_cast<float*>(b);
