@@ -132,13 +132,17 @@ conv2d_status_t conv2d_selected(const conv2d_params_t* p, conv2d_algo_t* chosen)
  * Fails with CONV2D_ERR_UNSUPPORTED if `algo` cannot run `p`. */
 conv2d_status_t conv2d_set_selected(const conv2d_params_t* p, conv2d_algo_t algo);
 
-/* Tuned parameter variant of the implicit_gemm / matmul_1x1 kernels for `p` (the "/variant" of the
- * selection table below; a bit mask: A-operand path, N tile, B path, K split -- igemm.cu).
+/* Tuned parameter variant of the implicit_gemm / matmul_1x1 / winograd_f2x2_3x3 kernels for `p` ("different
+ * parameters for each algorithm"; the "/variant" of the selection table below).
+ * implicit_gemm / matmul_1x1: a bit mask -- A-operand path, N tile, B path, K split (igemm.cu).
+ * winograd_f2x2_3x3: 0 = transform kernels + batched tcgen05 GEMM (winograd.cu), 1 = the fused kernel
+ * (input transform, 16 coordinate GEMMs and output transform in one cluster-of-2 launch; wino_fused.cu),
+ * enumerated where C % 4 == 0, F % 4 == 0 and Ho >= 2.
  * get: *variant = the variant conv2d_autotune / load_selection / set_variant recorded, or 0 (the
  * default parameters) if none was.  set: seeds it (e.g. replaying rank 0's tuned choice on every rank);
  * CONV2D_ERR_INVALID_PARAMS unless `variant` is one the auto-selector enumerates for `p` and `algo`.
- * `algo` must be CONV2D_ALGO_IMPLICIT_GEMM or CONV2D_ALGO_MATMUL_1X1 (CONV2D_ERR_INVALID_PARAMS
- * otherwise; CONV2D_ERR_UNSUPPORTED if it cannot run `p`).  Host-only. */
+ * `algo` must be one of those three (CONV2D_ERR_INVALID_PARAMS otherwise; CONV2D_ERR_UNSUPPORTED if it cannot
+ * run `p`).  Host-only. */
 conv2d_status_t conv2d_get_variant(const conv2d_params_t* p, conv2d_algo_t algo, int* variant);
 conv2d_status_t conv2d_set_variant(const conv2d_params_t* p, conv2d_algo_t algo, int variant);
 
@@ -172,7 +176,8 @@ conv2d_status_t conv2d_set_autotune_flush(void* buf, size_t bytes);
 /* Persisted selector table ("table serialization round-trips", SPEC.md:354's line format with
  * this library's full cache key).  One line per cached choice of the current device:
  *     N H W C F KH KW SH SW same|valid fp32|tf32 : algorithm[/variant]
- * (variant = the tuned algorithm parameters of implicit_gemm / matmul_1x1, see igemm.cu), then
+ * (variant = the tuned algorithm parameters of implicit_gemm / matmul_1x1 / winograd_f2x2_3x3, see
+ * conv2d_get_variant), then
  * `default : a,b,...` (algorithms by number of entries won; informative) and `#` comments.
  * save: CONV2D_ERR_IO if the file cannot be written.  load: parses and validates every line first
  * (CONV2D_ERR_INVALID_PARAMS for malformed lines / unknown names / invalid params / a variant the

@@ -236,7 +236,8 @@ def conv2d_set_selected(p: Params, algo: int) -> None:
 
 
 def conv2d_get_variant(p: Params, algo: int) -> int:
-    """Tuned parameter variant of implicit_gemm / matmul_1x1 for p (0 = defaults; include/conv2d.h)."""
+    """Tuned parameter variant of implicit_gemm / matmul_1x1 / winograd_f2x2_3x3 for p (0 = defaults;
+    include/conv2d.h)."""
     v = ctypes.c_int()
     _check(_lib.conv2d_get_variant(ctypes.byref(p.c()), int(algo), ctypes.byref(v)), "conv2d_get_variant")
     return int(v.value)
@@ -249,7 +250,7 @@ def conv2d_set_variant(p: Params, algo: int, variant: int) -> None:
 def conv2d_variants(p: Params, algo: int) -> list:
     """The parameter variants the auto-selector enumerates for (p, algo): exactly those conv2d_set_variant
     accepts (probes 0..31, restores the recorded variant)."""
-    if algo not in (ALGO_IMPLICIT_GEMM, ALGO_MATMUL_1X1):
+    if algo not in (ALGO_IMPLICIT_GEMM, ALGO_MATMUL_1X1, ALGO_WINOGRAD_F2X2_3X3):
         return [0]
     keep = conv2d_get_variant(p, algo)
     out = []

@@ -135,6 +135,31 @@ int algo_launches(const Problem& q, conv2d_algo_t a) {
   }
 }
 
+// ---- tuned parameter variants ("different parameters for each algorithm"):
+// implicit_gemm / matmul_1x1 (igemm.cu: A path, N tile, B path, K split) and winograd_f2x2_3x3 (winograd.cu:
+// 0 = transforms + batched GEMM, 1 = the fused kernel of wino_fused.cu)
+bool has_variants(conv2d_algo_t a) {
+  return a == CONV2D_ALGO_IMPLICIT_GEMM || a == CONV2D_ALGO_MATMUL_1X1 || a == CONV2D_ALGO_WINOGRAD_F2X2_3X3;
+}
+int algo_variants(const Problem& q, conv2d_algo_t a, int* masks) {
+  if (a == CONV2D_ALGO_WINOGRAD_F2X2_3X3) return winograd_variants(q, masks);
+  if (a == CONV2D_ALGO_IMPLICIT_GEMM || a == CONV2D_ALGO_MATMUL_1X1)
+    return igemm_variants(q, a == CONV2D_ALGO_MATMUL_1X1, masks);
+  masks[0] = 0;
+  return 1;
+}
+void algo_set_variant(const Problem& q, conv2d_algo_t a, int v) {
+  if (a == CONV2D_ALGO_WINOGRAD_F2X2_3X3) winograd_set_variant(q, v);
+  else if (a == CONV2D_ALGO_IMPLICIT_GEMM || a == CONV2D_ALGO_MATMUL_1X1)
+    igemm_set_variant(q, a == CONV2D_ALGO_MATMUL_1X1, v);
+}
+bool algo_get_variant(const Problem& q, conv2d_algo_t a, int* v) {
+  if (a == CONV2D_ALGO_WINOGRAD_F2X2_3X3) return winograd_get_variant(q, v);
+  if (a == CONV2D_ALGO_IMPLICIT_GEMM || a == CONV2D_ALGO_MATMUL_1X1)
+    return igemm_get_variant(q, a == CONV2D_ALGO_MATMUL_1X1, v);
+  return false;
+}
+
 // ---- device check (sm_100 only: the kernels are built for sm_100a exclusively)
 std::mutex g_dev_mu;
 std::map<int, bool> g_dev_ok;
@@ -242,16 +267,15 @@ conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int de
     const conv2d_algo_t a = (conv2d_algo_t)ai;
     if (!algo_supports(q, a)) continue;
     // algorithm parameters: time every variant of the algorithm, keep its best
-    const bool gemm_like = a == CONV2D_ALGO_IMPLICIT_GEMM || a == CONV2D_ALGO_MATMUL_1X1;
-    const bool is_1x1 = a == CONV2D_ALGO_MATMUL_1X1;
+    const bool tuned = has_variants(a);
     int masks[32] = {0};
-    const int nvar = gemm_like ? igemm_variants(q, is_1x1, masks) : 1;
+    const int nvar = algo_variants(q, a, masks);
     double t_best = 1e300;
     int v_best = 0;
     for (int vi = 0; vi < nvar && st == CONV2D_OK; ++vi) {
       const int v = masks[vi];
       if (!measured(ai, v)) continue;
-      if (gemm_like) igemm_set_variant(q, is_1x1, v);
+      if (tuned) algo_set_variant(q, a, v);
       st = run_algo(q, a, in, filt, out, ws, s);
       if (st == CONV2D_ERR_CUDA) {
         // a measurement failure drops that candidate and logs a warning.  Only a launch that
@@ -293,7 +317,7 @@ conv2d_status_t autotune_impl(const conv2d_params_t* p, const Problem& q, int de
     }
     if (st != CONV2D_OK) break;
     if (t_best >= 1e299) continue;  // hybrid: no variant of this algorithm was timed
-    if (gemm_like) igemm_set_variant(q, is_1x1, v_best);
+    if (tuned) algo_set_variant(q, a, v_best);
     g_tune_times[ai] = t_best * 1000.0;
     if (t_best < best_t) {  // strict: ties keep the earlier enum
       best_t = t_best;
@@ -343,9 +367,8 @@ static void selector_features(const conv2d_params_t* p, const Problem& q, double
 }
 
 static bool variant_enumerated(const Problem& q, conv2d_algo_t a, int v) {
-  if (a != CONV2D_ALGO_IMPLICIT_GEMM && a != CONV2D_ALGO_MATMUL_1X1) return v == 0;
   int masks[32];
-  const int n = igemm_variants(q, a == CONV2D_ALGO_MATMUL_1X1, masks);
+  const int n = algo_variants(q, a, masks);
   for (int i = 0; i < n; ++i)
     if (masks[i] == v) return true;
   return false;
@@ -486,7 +509,7 @@ conv2d_status_t conv2d_forward(const conv2d_params_t* p, conv2d_algo_t algo, con
     if (!hit && g_auto_policy.load() == CONV2D_AUTO_PREDICT) {  // learned choice: no timing, capture-safe
       int v = 0;
       selector_predict(p, q, &a, &v);
-      if (a == CONV2D_ALGO_IMPLICIT_GEMM || a == CONV2D_ALGO_MATMUL_1X1) igemm_set_variant(q, a == CONV2D_ALGO_MATMUL_1X1, v);
+      algo_set_variant(q, a, v);
       std::lock_guard<std::mutex> lk(g_cache_mu);
       g_cache[key_of(p, dev)] = a;
     } else if (!hit) {
@@ -554,8 +577,8 @@ conv2d_status_t conv2d_set_selected(const conv2d_params_t* p, conv2d_algo_t algo
 static conv2d_status_t variant_problem(const conv2d_params_t* p, conv2d_algo_t algo, Problem* q) {
   std::string why;
   if (!shape_of(p, q, &why)) return fail(CONV2D_ERR_INVALID_PARAMS, why);
-  if (algo != CONV2D_ALGO_IMPLICIT_GEMM && algo != CONV2D_ALGO_MATMUL_1X1)
-    return fail(CONV2D_ERR_INVALID_PARAMS, "variants exist for implicit_gemm / matmul_1x1 only");
+  if (!has_variants(algo))
+    return fail(CONV2D_ERR_INVALID_PARAMS, "variants exist for implicit_gemm / matmul_1x1 / winograd_f2x2_3x3 only");
   if (!algo_supports(*q, algo)) return fail(CONV2D_ERR_UNSUPPORTED, "algorithm does not support these params");
   return CONV2D_OK;
 }
@@ -567,7 +590,7 @@ conv2d_status_t conv2d_get_variant(const conv2d_params_t* p, conv2d_algo_t algo,
   const conv2d_status_t st = variant_problem(p, algo, &q);
   if (st != CONV2D_OK) return st;
   int v = 0;
-  if (igemm_get_variant(q, algo == CONV2D_ALGO_MATMUL_1X1, &v)) *variant = v;
+  if (algo_get_variant(q, algo, &v)) *variant = v;
   return CONV2D_OK;
 }
 
@@ -575,12 +598,11 @@ conv2d_status_t conv2d_set_variant(const conv2d_params_t* p, conv2d_algo_t algo,
   Problem q;
   const conv2d_status_t st = variant_problem(p, algo, &q);
   if (st != CONV2D_OK) return st;
-  const bool is_1x1 = algo == CONV2D_ALGO_MATMUL_1X1;
   int masks[32];
-  const int n = igemm_variants(q, is_1x1, masks);
+  const int n = algo_variants(q, algo, masks);
   for (int i = 0; i < n; ++i)
     if (masks[i] == variant) {
-      igemm_set_variant(q, is_1x1, variant);
+      algo_set_variant(q, algo, variant);
       return CONV2D_OK;
     }
   return fail(CONV2D_ERR_INVALID_PARAMS, "variant " + std::to_string(variant) + " is not enumerated for these params");
@@ -630,8 +652,7 @@ conv2d_status_t conv2d_save_selection(const char* path) {
     Problem q;
     std::string why;
     int v = 0;
-    if ((kv.second == CONV2D_ALGO_IMPLICIT_GEMM || kv.second == CONV2D_ALGO_MATMUL_1X1) && shape_of(&p, &q, &why) &&
-        igemm_get_variant(q, kv.second == CONV2D_ALGO_MATMUL_1X1, &v))
+    if (has_variants(kv.second) && shape_of(&p, &q, &why) && algo_get_variant(q, kv.second, &v))
       fprintf(f, "/%d", v);
     fprintf(f, "\n");
     ++wins[kv.second];
@@ -761,14 +782,14 @@ conv2d_status_t conv2d_load_selection(const char* path, int* loaded) {
       why = std::string(conv2d_algo_name(e.a)) + " does not support these params";
       break;
     }
-    if (e.variant >= 0 && e.a != CONV2D_ALGO_IMPLICIT_GEMM && e.a != CONV2D_ALGO_MATMUL_1X1) {
+    if (e.variant >= 0 && !has_variants(e.a)) {
       st = CONV2D_ERR_INVALID_PARAMS;
-      why = "a variant is only defined for implicit_gemm / matmul_1x1";
+      why = "a variant is only defined for implicit_gemm / matmul_1x1 / winograd_f2x2_3x3";
       break;
     }
     if (e.variant >= 0) {  // only the variants the auto-selector enumerates for these params (as set_variant)
       int masks[32];
-      const int n = igemm_variants(q, e.a == CONV2D_ALGO_MATMUL_1X1, masks);
+      const int n = algo_variants(q, e.a, masks);
       bool found = false;
       for (int i = 0; i < n; ++i) found = found || masks[i] == e.variant;
       if (!found) {
@@ -790,7 +811,7 @@ conv2d_status_t conv2d_load_selection(const char* path, int* loaded) {
       Problem q;
       std::string w;
       shape_of(&e.p, &q, &w);
-      igemm_set_variant(q, e.a == CONV2D_ALGO_MATMUL_1X1, e.variant);
+      algo_set_variant(q, e.a, e.variant);
     }
   if (loaded) *loaded = (int)entries.size();
   return CONV2D_OK;

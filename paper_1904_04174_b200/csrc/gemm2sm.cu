@@ -931,13 +931,18 @@ bool gemm2_encode_tiled(CUtensorMap* m, int rank, const void* base, const uint64
 
 bool gemm2_encode_tiled_sw(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
                            const uint32_t* box, int swizzle) {
+  return gemm2_encode_tiled_es(m, rank, base, dims, strides, box, nullptr, swizzle);
+}
+
+bool gemm2_encode_tiled_es(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
+                           const uint32_t* box, const uint32_t* elem_strides, int swizzle) {
   if (load_driver_fns() != cudaSuccess) return false;
   cuuint64_t d[5], st[4];
   cuuint32_t b[5], es[5];
   for (int i = 0; i < rank; ++i) {
     d[i] = dims[i];
     b[i] = box[i];
-    es[i] = 1;
+    es[i] = elem_strides ? elem_strides[i] : 1;
     if (i < rank - 1) st[i] = strides[i];
   }
   return g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), d, st, b, es,

@@ -61,6 +61,9 @@ cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_
                              int64_t npad, int block_n, float* out, cudaStream_t s);
 bool gemm2_encode_tiled_sw(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
                            const uint32_t* box, int swizzle);  // swizzle: a CUtensorMapSwizzle value
+// same with TMA traversal strides (elem_strides[i] in [1, 8]; dimension i then loads ceil(box[i] / stride) elements)
+bool gemm2_encode_tiled_es(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
+                           const uint32_t* box, const uint32_t* elem_strides, int swizzle);
 int gemm2_choose_block_n(int64_t N);
 // remainder-split factor for `tiles` pair tiles of nkb k-blocks (0 = not applicable)
 int gemm2_rsplit_factor(int64_t tiles, int nkb);

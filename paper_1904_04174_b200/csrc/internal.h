@@ -51,13 +51,17 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
 size_t winograd_workspace(const Problem& p, int mt);  // mt = output tile: 2 (F2x2) or 4 (F4x4)
 int winograd_launches(const Problem& p, int mt);
 int winograd_splits(const Problem& p, int mt);  // K-split count of the batched GEMMs (1 = none)
+// F(2x2) parameter variants (0 = transforms + batched GEMM, 1 = fused kernel where wino_fused_ok)
+int winograd_variants(const Problem& p, int* masks);
+bool winograd_get_variant(const Problem& p, int* v);  // false if never set
+void winograd_set_variant(const Problem& p, int v);
 cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const float* filt, float* out, void* ws,
                             cudaStream_t s);
 // filter transform U = G g G^T into Ut[xi][fpad][cpad] (hi, and lo when three_x; TF32: rna-rounded hi)
 cudaError_t launch_wino_filter(int mt, const float* w, int C, int F, int64_t cpad, int64_t fpad, float* ut_hi,
                                float* ut_lo, bool three_x, cudaStream_t s);
 // ---- wino_fused.cu: F(2x2,3x3) with the input transform, the 16 coordinate GEMMs and the output transform in
-// one cluster kernel (V and M never leave the SM pair); the default F(2x2) path where wino_fused_ok
+// one cluster kernel (V and M never leave the SM pair): F(2x2) parameter variant 1 where wino_fused_ok
 bool wino_fused_ok(const Problem& p);
 size_t wino_fused_workspace(const Problem& p);
 cudaError_t launch_wino_fused(const Problem& p, const float* in, const float* filt, float* out, void* ws,

@@ -16,12 +16,16 @@
 //
 // Tiles: T = N * ceil(Ho/2) * ceil(Wo/2); odd Ho/Wo extend the grid with zero input and
 // the surplus outputs are discarded.  Multiplies per 2x2 output tile: 16 vs 36 direct.
-// Round-1 form: transforms are separate CUDA-core kernels with V and M staged in the
-// workspace (the GEMMs run on the tensor cores); the fused form is DESIGN.md "Next".
+// This file: the transforms as separate bandwidth kernels with V and M staged in the workspace and the
+// GEMMs on the tensor cores (parameter variant 0).  F(2x2) variant 1 is the fused kernel (wino_fused.cu);
+// the auto-selector times both per layer.
 // TF32 mode rounds U and V to TF32 with cvt.rna (reading R16); FP32 mode runs the GEMMs
 // in 3xTF32.
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "gemm2sm.h"
 #include "launch.cuh"
@@ -338,7 +342,42 @@ __global__ void __launch_bounds__(128) wino_filter_kernel(const float* __restric
   wino_filter_tile<MT>(w, C, F, cpad, fpad, ut_hi, ut_lo, mode, (int)blockIdx.x % nfx, (int)blockIdx.x / nfx);
 }
 
+// F(2x2) parameter variant (the auto-selector times both): 0 = the transform kernels +
+// batched GEMM below, 1 = the fused kernel (wino_fused.cu).  Default 0: the fused kernel is shared-memory-port
+// bound with 32-feature MMAs, so it wins only on some shapes.
+using WVKey = std::tuple<int, int, int, int, int, int, int, int, int, int, int>;
+std::mutex g_wvmu;
+std::map<WVKey, int> g_wvariant;
+WVKey wvkey(const Problem& p) {
+  return WVKey(p.N, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH, p.SW, p.pad_top * 64 + p.pad_left, (int)p.math);
+}
+int wvariant_of(const Problem& p) {
+  if (const char* f = getenv("CONV2D_FORCE_WINO_VARIANT")) return atoi(f) & 1;  // parity-test hook
+  std::lock_guard<std::mutex> lk(g_wvmu);
+  auto it = g_wvariant.find(wvkey(p));
+  return it == g_wvariant.end() ? 0 : it->second;
+}
+bool use_fused(const Problem& p, int mt) { return mt == 2 && wvariant_of(p) == 1 && wino_fused_ok(p); }
+
 }  // namespace
+
+int winograd_variants(const Problem& p, int* masks) {
+  masks[0] = 0;
+  if (!wino_fused_ok(p)) return 1;
+  masks[1] = 1;
+  return 2;
+}
+bool winograd_get_variant(const Problem& p, int* v) {
+  std::lock_guard<std::mutex> lk(g_wvmu);
+  auto it = g_wvariant.find(wvkey(p));
+  if (it == g_wvariant.end()) return false;
+  *v = it->second;
+  return true;
+}
+void winograd_set_variant(const Problem& p, int v) {
+  std::lock_guard<std::mutex> lk(g_wvmu);
+  g_wvariant[wvkey(p)] = v;
+}
 
 cudaError_t launch_wino_filter(int mt, const float* w, int C, int F, int64_t cpad, int64_t fpad, float* ut_hi,
                                float* ut_lo, bool three_x, cudaStream_t s) {
@@ -352,15 +391,15 @@ size_t winograd_workspace(const Problem& p, int mt) {
   return mt == 2 ? std::max(unfused, wino_fused_workspace(p)) : unfused;
 }
 int winograd_launches(const Problem& p, int mt) {
-  if (mt == 2 && wino_fused_ok(p)) return 2;
+  if (use_fused(p, mt)) return 2;
   return 3 + (make_wplan(p, mt).splits > 1 ? 1 : 0);
 }
-int winograd_splits(const Problem& p, int mt) { return mt == 2 && wino_fused_ok(p) ? 1 : make_wplan(p, mt).splits; }
+int winograd_splits(const Problem& p, int mt) { return use_fused(p, mt) ? 1 : make_wplan(p, mt).splits; }
 
 cudaError_t launch_winograd(const Problem& p, int mt, const float* in, const float* filt, float* out, void* ws,
                             cudaStream_t s) {
-  // F(2x2): the fused kernel (wino_fused.cu) whenever its plan applies and the pointers are TMA-aligned
-  if (mt == 2 && wino_fused_ok(p) && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0)
+  // F(2x2) variant 1: the fused kernel (wino_fused.cu), when the pointers are TMA-aligned
+  if (use_fused(p, mt) && ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0)
     return launch_wino_fused(p, in, filt, out, ws, s);
   const WPlan w = make_wplan(p, mt);
   uint8_t* b = static_cast<uint8_t*>(ws);

@@ -392,6 +392,41 @@ def test_algorithm_parameter_variants(cuda_ok, monkeypatch, variant, case):
             assert_int_exact(p, gpu_conv(p, xi, wi, a), refi, deni, a, f"variant int {case} {a}")
 
 
+WINO_FUSED_CASES = [l.params(1) for l in ALL_SHAPES if l.window == 3 and l.stride == 1 and l.channels >= 32] + [
+    dict(batch=3, in_rows=15, in_cols=9, channels=64, features=68, window_rows=3, window_cols=3, stride_rows=1,
+         stride_cols=1, padding=1),    # VALID, ragged tile blocks, F % 32 != 0
+    dict(batch=1, in_rows=9, in_cols=7, channels=40, features=36, window_rows=3, window_cols=3, stride_rows=1,
+         stride_cols=1, padding=0),    # odd Ho / Wo, C % 16 != 0
+    dict(batch=9, in_rows=7, in_cols=7, channels=32, features=96, window_rows=3, window_cols=3, stride_rows=1,
+         stride_cols=1, padding=0),    # whole images per tile block (NB = 8) plus a ragged block
+    dict(batch=5, in_rows=28, in_cols=28, channels=128, features=128, window_rows=3, window_cols=3,
+         stride_rows=1, stride_cols=1, padding=0),  # several units per cluster
+    dict(batch=2, in_rows=2, in_cols=30, channels=32, features=32, window_rows=3, window_cols=3, stride_rows=1,
+         stride_cols=1, padding=0),    # a single tile row (Ho = 2)
+]
+
+
+@pytest.mark.parametrize("case", WINO_FUSED_CASES, ids=lambda d: "x".join(str(v) for v in d.values()))
+def test_winograd_fused_variant(cuda_ok, monkeypatch, case):
+    """winograd_f2x2_3x3 variant 1 (the fused kernel, wino_fused.cu) on every paper 3x3/s1 shape and the
+    block-geometry edge cases: bit-exact in the integer regime (P7), within tolerance and under the P10
+    ceiling on uniform data, both math modes; and bitwise equal to itself run again (determinism)."""
+    monkeypatch.setenv("CONV2D_FORCE_WINO_VARIANT", "1")
+    p0 = C().Params(**case)
+    a = C().ALGO_WINOGRAD_F2X2_3X3
+    assert 1 in C().conv2d_variants(p0, a)
+    x, w = make_inputs(p0, layer_id=950)
+    ref, den = O.conv2d(oparams(p0), x, w, with_denom=True)
+    xi, wi = make_inputs(p0, layer_id=951, dist=synth.DIST_INT5)
+    refi, deni = O.conv2d(oparams(p0), xi, wi, with_denom=True)
+    for math in MATHS:
+        p = p0.replace(math=math)
+        y = gpu_conv(p, x, w, a)
+        check_close(p, y, ref, den, a, f"fused {case} math={math}")
+        assert np.array_equal(y, gpu_conv(p, x, w, a)), "fused winograd not deterministic"
+        assert_int_exact(p, gpu_conv(p, xi, wi, a), refi, deni, a, f"fused int {case} math={math}")
+
+
 def test_selection_table_gpu_round_trip(cuda_ok, tmp_path):
     """N4: the tuned choice (algorithm + its parameter variant) survives save -> clear -> load, and
     conv2d_forward(AUTO) then runs the loaded choice without tuning (same bits)."""

@@ -178,6 +178,27 @@ def test_variant_get_set_host_side(C):
     assert e.value.status == C.ERR_UNSUPPORTED
 
 
+def test_winograd_f2x2_variants_host_side(C):
+    """winograd_f2x2_3x3 parameter variants: 0 = transforms + batched GEMM, 1 = the fused kernel
+    (wino_fused.cu), enumerated only where its TMA plan applies (C % 4 == 0, F % 4 == 0, Ho >= 2)."""
+    W = C.ALGO_WINOGRAD_F2X2_3X3
+    for math in (C.MATH_FP32, C.MATH_TF32):
+        p = C.Params(2, 14, 14, 256, 256, 3, 3, math=math)  # R17-like
+        assert C.conv2d_variants(p, W) == [0, 1]
+        C.conv2d_set_variant(p, W, 1)
+        assert C.conv2d_get_variant(p, W) == 1
+        C.conv2d_set_variant(p, W, 0)
+        assert C.conv2d_get_variant(p, W) == 0
+        with pytest.raises(C.Conv2dError) as e:
+            C.conv2d_set_variant(p, W, 2)
+        assert e.value.status == C.ERR_INVALID_PARAMS
+    # C % 4 != 0 (the halo boxes need 16-byte pixel strides) and a 1-row output: only the unfused form
+    assert C.conv2d_variants(C.Params(1, 9, 7, 34, 36, 3, 3), W) == [0]
+    assert C.conv2d_variants(C.Params(1, 1, 9, 32, 32, 3, 3), W) == [0]
+    # the fused form needs only the filter transform in the workspace (16 x Fpad x Cpad hi + lo)
+    assert C.conv2d_query_workspace(C.Params(2, 14, 14, 256, 256, 3, 3), W) >= 2 * 16 * 256 * 256 * 4
+
+
 @pytest.mark.parametrize("case", [(2, 13, 11, 5, 3, 3, 2, 2, 0), (256, 112, 112, 64, 3, 3, 2, 2, 0),
                                   (3, 14, 14, 4, 2, 2, 2, 2, 1), (1, 9, 10, 3, 4, 2, 3, 1, 0),
                                   (32, 7, 7, 2048, 7, 7, 1, 1, 1)], ids=str)
