@@ -445,25 +445,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                                : AMODE == A_NARROW ? umma_desc_interleave_kmajor(smem_u32(a_lo(l)), 2048, 128)
                                                    : umma_desc_sw128_kmajor(smem_u32(a_lo(l)));
           const uint64_t dbl = THREE_X ? bdesc(BRES ? res_lo(kb) : b_lo(s)) : 0;
-#pragma unroll
-          for (int k = 0; k < BK / 8; ++k) {
-            const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);
-            const uint64_t adv_b = bmn ? (uint64_t)((k * 1024) >> 4) : adv;
-            // narrow A: one K=8 step = two 16-byte core-matrix columns = 2 boxes = 4 KB
-            const uint64_t adv_a = AMODE == A_NARROW ? (uint64_t)((k * 4096) >> 4) : adv;
-            const uint32_t accum = (kb > tl.kb0 || k > 0) ? 1u : 0u;
-            if (THREE_X && C_::LO_TMEM) {
-              mma_tf32_2sm_ts_warp(d, lo_t + (uint32_t)(k * 8), dbh + adv_b, idesc, accum);
-              mma_tf32_2sm_warp(d, dah + adv_a, dbl + adv_b, idesc, 1u);
-              mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv_b, idesc, 1u);
-            } else if (THREE_X) {
-              mma_tf32_2sm_warp(d, dal + adv_a, dbh + adv_b, idesc, accum);
-              mma_tf32_2sm_warp(d, dah + adv_a, dbl + adv_b, idesc, 1u);
-              mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv_b, idesc, 1u);
-            } else {
-              mma_tf32_2sm_warp(d, dah + adv_a, dbh + adv_b, idesc, accum);
-            }
-          }
+          // the k-block's four K=8 steps from one asm block (sm100.cuh mma2_kblock_*): descriptors advance 32 B
+          // per step (MN-major B: 1 KB; narrow A: two 16-byte core-matrix columns = 2 boxes = 4 KB)
+          static_assert(BK == 32, "mma2_kblock_* issue four K=8 steps");
+          const uint64_t a_step = AMODE == A_NARROW ? (uint64_t)(4096 >> 4) : (uint64_t)(32 >> 4);
+          const uint64_t b_step = bmn ? (uint64_t)(1024 >> 4) : (uint64_t)(32 >> 4);
+          const uint32_t acc0 = kb > tl.kb0 ? 1u : 0u;
+          if (THREE_X && C_::LO_TMEM)
+            mma2_kblock_3x_ts(d, lo_t, dah, dbh, dbl, a_step, b_step, idesc, acc0);
+          else if (THREE_X)
+            mma2_kblock_3x_ss(d, dah, dal, dbh, dbl, a_step, b_step, idesc, acc0);
+          else
+            mma2_kblock_1x_ss(d, dah, dbh, a_step, b_step, idesc, acc0);
           mma_commit_2sm_mc_warp(&empty[s], 0x3);
           if (THREE_X && !C_::LO_TMEM) mma_commit_2sm_mc_warp(&lo_empty[l], 0x3);
         }

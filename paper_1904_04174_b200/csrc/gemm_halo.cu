@@ -316,19 +316,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               const uint64_t dbx = umma_desc_sw128_kmajor(smem_u32(b_x(s)));
               const uint64_t dbz = C_::CONCAT ? umma_desc_sw128_kmajor(smem_u32(b_z(s))) : 0;
               const uint64_t dbl = C_::CONCAT ? 0 : umma_desc_sw128_kmajor(smem_u32(b_lo(s)));
-#pragma unroll
-              for (int k = 0; k < BK / 8; ++k) {
-                const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);
-                const uint32_t accum = (cb > 0 || kb > 0 || k > 0) ? 1u : 0u;
-                if (C_::CONCAT) {
-                  mma_tf32_2sm_ts_warp(d, ahi + (uint32_t)(k * 8), dbz + adv, idesc2, accum);
-                  mma_tf32_2sm_ts_warp(d, alo + (uint32_t)(k * 8), dbx + adv, idesc, 1u);
-                } else {
-                  mma_tf32_2sm_ts_warp(d, alo + (uint32_t)(k * 8), dbx + adv, idesc, accum);
-                  mma_tf32_2sm_ts_warp(d, ahi + (uint32_t)(k * 8), dbl + adv, idesc, 1u);
-                  mma_tf32_2sm_ts_warp(d, ahi + (uint32_t)(k * 8), dbx + adv, idesc, 1u);
-                }
-              }
+              // the tap's four K=8 steps from one asm block (sm100.cuh mma2_kblock_tt_*)
+              const uint32_t acc0 = (cb > 0 || kb > 0) ? 1u : 0u;
+              if (C_::CONCAT)
+                mma2_kblock_tt_concat(d, ahi, alo, dbz, dbx, idesc2, idesc, acc0);
+              else
+                mma2_kblock_tt_3x(d, ahi, alo, dbx, dbl, idesc, acc0);
               if (!C_::BRES) mma_commit_2sm_mc_warp(&b_empty[s], 0x3);
               mma_commit_2sm_mc_warp(&a_empty[slot], 0x3);
               ++ait;
@@ -340,6 +333,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             const uint64_t dbx = umma_desc_sw128_kmajor(smem_u32(b_x(s)));
             const uint64_t dbz = C_::CONCAT ? umma_desc_sw128_kmajor(smem_u32(b_z(s))) : 0;
             const uint64_t dbl = (THREE_X && !C_::CONCAT) ? umma_desc_sw128_kmajor(smem_u32(b_lo(s))) : 0;
+            if constexpr (GEOM == G3X3 && !THREE_X) {  // TF32 3x3: one asm block per k-block (sm100.cuh)
+              mma2_kblock_1x_ss(d, dah0, dbx, 2, 2, idesc, (cb > 0 || kb > 0) ? 1u : 0u);
+              if (!C_::BRES) mma_commit_2sm_mc_warp(&b_empty[s], 0x3);
+              continue;
+            }
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
               const uint64_t adv = (uint64_t)((k * 8 * 4) >> 4);  // B: 32 bytes per K=8 step

@@ -500,3 +500,127 @@ __device__ __forceinline__ void mma_tf32_2sm_ts_warp(uint32_t d_tmem, uint32_t a
       : "memory");
 }
 }  // namespace sm100
+
+namespace sm100 {
+// ---- one 32-wide k-block (four K=8 steps) of cta_group::2 MMAs issued from ONE asm block with a single elect.
+// Per-MMA warp-collective wrappers each cost an ELECT / R2UR / VOTEU dependency chain of ~60-70 cycles
+// (measured with clock64 in wino_fused.cu); an M=256 x N<=128 x K=8 MMA executes in 32-64 cycles per SM, so
+// issue, not the tensor pipe, bounded N <= 128 tiles (R4 halo: tensor pipe 61% active, transform warps
+// waiting on the MMA warp, profiles/round2_ncu.md).  Descriptors advance by a_step / b_step (16-byte units)
+// per K step; the first MMA of the block accumulates iff acc0, all later ones always do.
+__device__ __forceinline__ void mma2_kblock_3x_ss(uint32_t d, uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl,
+                                                  uint64_t a_step, uint64_t b_step, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 ah, al, bh, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %8, 0;\n\tsetp.eq.u32 t, 0, 0;\n\t"
+      "mov.b64 ah, %1;\n\tmov.b64 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], al, bh, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bl, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %7, t;\n\t"
+      "add.u64 ah, ah, %5;\n\tadd.u64 al, al, %5;\n\tadd.u64 bh, bh, %6;\n\tadd.u64 bl, bl, %6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], al, bh, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bl, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %7, t;\n\t"
+      "add.u64 ah, ah, %5;\n\tadd.u64 al, al, %5;\n\tadd.u64 bh, bh, %6;\n\tadd.u64 bl, bl, %6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], al, bh, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bl, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %7, t;\n\t"
+      "add.u64 ah, ah, %5;\n\tadd.u64 al, al, %5;\n\tadd.u64 bh, bh, %6;\n\tadd.u64 bl, bl, %6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], al, bh, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bl, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %7, t;\n\t"
+      "}" ::"r"(d), "l"(ah), "l"(al), "l"(bh), "l"(bl), "l"(a_step), "l"(b_step), "r"(idesc), "r"(acc0)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_kblock_3x_ts(uint32_t d, uint32_t alo_tmem, uint64_t ah, uint64_t bh, uint64_t bl,
+                                                  uint64_t a_step, uint64_t b_step, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 ah, bh, bl;\n\t.reg .b32 lt;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %8, 0;\n\tsetp.eq.u32 t, 0, 0;\n\t"
+      "mov.b32 lt, %1;\n\tmov.b64 ah, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [lt], bh, %7, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bl, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %7, t;\n\t"
+      "add.u32 lt, lt, 8;\n\tadd.u64 ah, ah, %5;\n\tadd.u64 bh, bh, %6;\n\tadd.u64 bl, bl, %6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [lt], bh, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bl, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %7, t;\n\t"
+      "add.u32 lt, lt, 8;\n\tadd.u64 ah, ah, %5;\n\tadd.u64 bh, bh, %6;\n\tadd.u64 bl, bl, %6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [lt], bh, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bl, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %7, t;\n\t"
+      "add.u32 lt, lt, 8;\n\tadd.u64 ah, ah, %5;\n\tadd.u64 bh, bh, %6;\n\tadd.u64 bl, bl, %6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [lt], bh, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bl, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %7, t;\n\t"
+      "}" ::"r"(d), "r"(alo_tmem), "l"(ah), "l"(bh), "l"(bl), "l"(a_step), "l"(b_step), "r"(idesc), "r"(acc0)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_kblock_1x_ss(uint32_t d, uint64_t ah, uint64_t bh, uint64_t a_step,
+                                                  uint64_t b_step, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 ah, bh;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\tsetp.eq.u32 t, 0, 0;\n\t"
+      "mov.b64 ah, %1;\n\tmov.b64 bh, %2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %5, p;\n\t"
+      "add.u64 ah, ah, %3;\n\tadd.u64 bh, bh, %4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %5, t;\n\t"
+      "add.u64 ah, ah, %3;\n\tadd.u64 bh, bh, %4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %5, t;\n\t"
+      "add.u64 ah, ah, %3;\n\tadd.u64 bh, bh, %4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], ah, bh, %5, t;\n\t"
+      "}" ::"r"(d), "l"(ah), "l"(bh), "l"(a_step), "l"(b_step), "r"(idesc), "r"(acc0)
+      : "memory");
+}
+// halo kernel, A (hi | lo) from TMEM: hi x [B_hi | B_lo] (N = 2 BN, idesc2, bz) then lo x B_hi (idesc, bx)
+__device__ __forceinline__ void mma2_kblock_tt_concat(uint32_t d, uint32_t ahi_tmem, uint32_t alo_tmem, uint64_t bz,
+                                                      uint64_t bx, uint32_t idesc2, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 bz, bx;\n\t.reg .b32 ah, al;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %7, 0;\n\tsetp.eq.u32 t, 0, 0;\n\t"
+      "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bz, %3;\n\tmov.b64 bx, %4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bz, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bx, %6, t;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.u64 bz, bz, 2;\n\tadd.u64 bx, bx, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bz, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bx, %6, t;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.u64 bz, bz, 2;\n\tadd.u64 bx, bx, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bz, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bx, %6, t;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.u64 bz, bz, 2;\n\tadd.u64 bx, bx, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bz, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bx, %6, t;\n\t"
+      "}" ::"r"(d), "r"(ahi_tmem), "r"(alo_tmem), "l"(bz), "l"(bx), "r"(idesc2), "r"(idesc), "r"(acc0)
+      : "memory");
+}
+// halo kernel, A (hi | lo) from TMEM, BN = 128: lo x B_hi, hi x B_lo, hi x B_hi
+__device__ __forceinline__ void mma2_kblock_tt_3x(uint32_t d, uint32_t ahi_tmem, uint32_t alo_tmem, uint64_t bx,
+                                                  uint64_t bl, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 bx, bl;\n\t.reg .b32 ah, al;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\tsetp.eq.u32 t, 0, 0;\n\t"
+      "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bx, %3;\n\tmov.b64 bl, %4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bx, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bl, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bx, %5, t;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.u64 bx, bx, 2;\n\tadd.u64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bx, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bl, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bx, %5, t;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.u64 bx, bx, 2;\n\tadd.u64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bx, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bl, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bx, %5, t;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.u64 bx, bx, 2;\n\tadd.u64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bx, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bl, %5, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bx, %5, t;\n\t"
+      "}" ::"r"(d), "r"(ahi_tmem), "r"(alo_tmem), "l"(bx), "l"(bl), "r"(idesc), "r"(acc0)
+      : "memory");
+}
+}  // namespace sm100

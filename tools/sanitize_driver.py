@@ -68,7 +68,7 @@ def main():
             for a in range(1, C.NUM_ALGOS):
                 if not C.conv2d_supports(p, a):
                     continue
-                if a in (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1):
+                if a in (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1, C.ALGO_WINOGRAD_F2X2_3X3):
                     for v in C.conv2d_variants(p, a):
                         fails += not run(p, a, x, w, v)
                 else:
