@@ -369,6 +369,8 @@ def test_tf32_mma_reads_truncated_operands(cuda_ok):
 @pytest.mark.parametrize("case", [(2, 28, 28, 64, 64, 3, 3, 1, 1, 0), (1, 14, 15, 128, 128, 3, 3, 1, 1, 1),
                                   (2, 12, 12, 64, 256, 1, 1, 1, 1, 0), (1, 9, 9, 64, 320, 3, 3, 2, 2, 0),
                                   (2, 21, 19, 3, 36, 7, 7, 2, 2, 0),
+                                  # 3x3 / C = 3 (V1-like): row-segment boxes and the A_STEM halo path (bit 0)
+                                  (2, 20, 22, 3, 64, 3, 3, 1, 1, 0), (1, 17, 9, 2, 40, 3, 2, 1, 1, 1),
                                   # remainder split: 150 / 85 / 100 pair tiles (last wave 2 / 11 / 26 of 74)
                                   (2, 150, 128, 256, 64, 1, 1, 1, 1, 0), (5, 68, 64, 96, 128, 3, 3, 1, 1, 0),
                                   (8, 28, 28, 256, 1024, 1, 1, 1, 1, 0),
