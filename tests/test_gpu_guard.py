@@ -39,6 +39,10 @@ SHAPES = [
     (1, 13, 11, 5, 130, 3, 3, 2, 1, 0),
     (2, 33, 70, 3, 64, 3, 3, 1, 1, 0),       # V1-like small C for the tiled kernel's vector paths
     (1, 9, 9, 20, 24, 5, 5, 1, 1, 0),        # tiled generic (runtime KW) path, F % 16 != 0
+    # fused Winograd F(2x2) (winograd_f2x2_3x3 variant 1): ragged tile blocks / NB > 1 / odd Ho, F % 32 != 0
+    (3, 15, 9, 64, 68, 3, 3, 1, 1, 1),
+    (9, 7, 7, 32, 96, 3, 3, 1, 1, 0),
+    (1, 9, 7, 40, 36, 3, 3, 1, 1, 0),
 ]
 
 
@@ -94,7 +98,8 @@ def test_guard_bands_and_repeatability(cuda_ok, case):
         for a in range(1, c.NUM_ALGOS):
             if not c.conv2d_supports(p, a):
                 continue
-            for v in (c.conv2d_variants(p, a) if a in (c.ALGO_IMPLICIT_GEMM, c.ALGO_MATMUL_1X1) else [None]):
+            tuned = a in (c.ALGO_IMPLICIT_GEMM, c.ALGO_MATMUL_1X1, c.ALGO_WINOGRAD_F2X2_3X3)
+            for v in (c.conv2d_variants(p, a) if tuned else [None]):
                 y1 = _run(p, a, x, w, v, 0x7FC00000)  # quiet NaN
                 assert bool(torch.isfinite(y1).all()), f"{case} {c.ALGO_NAMES[a]} v={v}: unwritten outputs"
                 for poison in (0x7FC00001, 0x00000000, 0x7F800000):
@@ -103,5 +108,5 @@ def test_guard_bands_and_repeatability(cuda_ok, case):
                         f"{case} {c.ALGO_NAMES[a]} v={v} math={math}: run-to-run difference (race?)"
                 assert torch.equal(x, x0) and torch.equal(w, w0), f"{c.ALGO_NAMES[a]} v={v}: input modified"
                 check_close(p, y1.view(ref.shape).cpu().numpy(), ref, den, a, f"guard {case} {a} v={v} m={math}")
-            if a in (c.ALGO_IMPLICIT_GEMM, c.ALGO_MATMUL_1X1):
+            if tuned:
                 c.conv2d_set_variant(p, a, 0)
