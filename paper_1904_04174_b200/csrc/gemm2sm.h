@@ -6,7 +6,7 @@
 
 namespace conv2d {
 
-enum { A_IM2COL = 0, A_DENSE = 1, A_GATHER = 2, A_NARROW = 3, A_ROWSEG = 4, A_HALO = 5, A_STEM = 6, A_S2D = 7 };
+enum { A_IM2COL = 0, A_DENSE = 1, A_GATHER = 2, A_NARROW = 3, A_ROWSEG = 4, A_HALO = 5, A_STEM = 6, A_S2D = 7, A_C4 = 8 };
 
 struct Gemm2Args {
   int a_mode;              // A_IM2COL: a = NHWC input (C % 32 == 0), k = (r, s, c-block of 32)
@@ -54,6 +54,10 @@ bool gemm2_encode_tiled(CUtensorMap* m, int rank, const void* base, const uint64
 bool halo_ok(const Problem& p);
 // space-to-depth stem (gemm_halo.cu): K x K / stride 2, K in {7, 8}, C <= 4, F <= 128
 bool s2d_ok(const Problem& p);
+bool c4_ok(const Problem& p);
+size_t c4_workspace(const Problem& p, int block_n, bool three_x);
+cudaError_t launch_gemm_c4(const Problem& p, const float* in, const float* filt, int block_n, bool three_x, void* ws,
+                           float* out, cudaStream_t s);
 size_t s2d_workspace(const Problem& p, int block_n, bool three_x);
 cudaError_t launch_gemm_s2d(const Problem& p, const float* in, const float* filt, int block_n, bool three_x,
                             void* ws, float* out, cudaStream_t s);

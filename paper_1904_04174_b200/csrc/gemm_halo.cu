@@ -28,7 +28,6 @@ namespace {
 using namespace sm100;
 
 constexpr int BK = 32;
-constexpr int NTHREADS = 320;
 constexpr int TW = 8, TH = 16;            // CTA output tile (wo x ho) = 128 GEMM rows
 constexpr int HWD = 16;                   // halo box width (pixels) = 8-row group pitch
 
@@ -38,15 +37,28 @@ constexpr int HWD = 16;                   // halo box width (pixels) = 8-row gro
 //   GS2D (1): the space-to-depth stem: a 4x4 / stride-1 VALID conv over X' = s2d(x) with 16 channels
 //             (64-byte pixel rows, SWIZZLE_64B): halo box {16 ch, 16 w, 19 h}, two taps per 32-wide
 //             k-block, eight k-blocks.  (7x7 or 8x8 / stride 2 with C <= 4 maps onto it exactly.)
-enum { G3X3 = 0, GS2D = 1 };
+//   G3C4 (2): 3x3 / stride 1 with C <= 4 (VGG conv1_1): a halo of 4-channel pixels (16-byte rows, built by the
+//             transform warps from a raw TMA patch, zero channels past C).  A K=8 step covers two horizontally
+//             adjacent taps: the view of tap (r, s) is a no-swizzle K-major operand whose second 16-byte core
+//             matrix column (channels of tap s+1) starts ONE pixel later (LBO = 16 B; SBO = 16 halo pixels =
+//             one output row) -- overlapping views, no data replicated.  Six steps (r, s in {0, 2}; the s = 3
+//             half has zero B) = two k-blocks, against 16 for a 32-channel-padded tap.
+enum { G3X3 = 0, GS2D = 1, G3C4 = 2 };
 template <int GEOM>
 struct Geo {
   static constexpr int TAPW = GEOM == GS2D ? 4 : 3;     // taps per filter row
   static constexpr int HHT = TH + TAPW - 1;             // halo box height
-  static constexpr int ROWB = GEOM == GS2D ? 64 : 128;  // bytes per halo pixel
+  static constexpr int ROWB = GEOM == GS2D ? 64 : GEOM == G3C4 ? 16 : 128;  // bytes per halo pixel
   static constexpr int HALO_ROWS = HWD * HHT;
   static constexpr int HALO_BYTES = (HALO_ROWS * ROWB + 1023) / 1024 * 1024;
-  static constexpr int KB_PER_UNIT = GEOM == GS2D ? 8 : 9;  // 32-wide k-blocks per (tile, channel block)
+  static constexpr int KB_PER_UNIT = GEOM == GS2D ? 8 : GEOM == G3C4 ? 2 : 9;  // 32-wide k-blocks per unit
+  static constexpr bool RAWG = GEOM != G3X3;           // halo built from raw patches, K steps from a table
+  // epilogue warps: G3C4 tiles are short (six K=8 steps), so the per-tile epilogue chain (TMEM load ->
+  // smem stage -> proxy fence -> TMA store) is the critical path; two warps per TMEM lane quarter, each
+  // owning half the accumulator columns, halve it (measured on VGG conv1_1: the MMA warp waited on
+  // tmem_empty, the epilogue never on tmem_full)
+  static constexpr int EW = GEOM == G3C4 ? 8 : 4;
+  static constexpr int NT = (6 + EW) * 32;
 };
 
 struct HArgs {
@@ -77,6 +89,14 @@ constexpr int RAW_ROWS = 2 * (TH + 3);  // 38 input rows behind a 19-row s2d hal
 // coordinate 16-byte aligned, so the load starts at the aligned float below the patch origin
 __host__ __device__ constexpr int raw_row_floats(int c) { return 32 * c + 4; }
 constexpr int RAW_BYTES_MAX = RAW_ROWS * raw_row_floats(3) * 4;  // C <= 3: 15200 B
+// G3C4: 18 rows x 11 pixels (the views reach pixel wo_l + 3 + 7 = 10) x C floats, + up to 3 floats of
+// alignment slack, rounded to whole 16-byte TMA units
+constexpr int RAW_ROWS_C4 = TH + 2;
+__host__ __device__ constexpr int raw_row_floats_c4(int c) { return (11 * c + 3 + 3) / 4 * 4; }
+template <int GEOM> __host__ __device__ constexpr int raw_rows() { return GEOM == G3C4 ? RAW_ROWS_C4 : RAW_ROWS; }
+template <int GEOM> __host__ __device__ constexpr int raw_floats(int c) {
+  return GEOM == G3C4 ? raw_row_floats_c4(c) : raw_row_floats(c);
+}
 
 template <int BN, bool THREE_X, int GEOM>
 struct HCfg {
@@ -97,21 +117,29 @@ struct HCfg {
   static constexpr bool CONCAT = THREE_X && BN == 64;
   static constexpr int BSTAGE = CONCAT ? BFULL + BHALF : (THREE_X ? 2 : 1) * BHALF;
   static constexpr int ACC = CONCAT ? 2 * BN : BN;                     // TMEM columns per accumulator
-  static constexpr int EPI = 4 * 2 * 32 * 128;
-  static constexpr int RAWB = GEOM == GS2D ? RAW_BYTES_MAX : 0;          // raw-patch staging (one slot)
+  static constexpr int EPI = Geo<GEOM>::EW * 2 * 32 * 128;
+  static constexpr int RAWB = Geo<GEOM>::RAWG ? RAW_BYTES_MAX : 0;      // raw-patch staging
+  // raw-patch ring: G3C4 patches are small (18 rows x 48 floats at most), so four are in flight -- a single
+  // slot serialises every tile behind one TMA round trip (measured: 1.6 us per tile on VGG conv1_1)
+  static constexpr int NR = GEOM == G3C4 ? 4 : 1;
+  static constexpr int RAW_SLOT = GEOM == G3C4 ? (RAW_ROWS_C4 * raw_row_floats_c4(4) * 4 + 127) / 128 * 128 : 0;
+  static_assert(NR * RAW_SLOT <= RAWB, "raw ring");
   static constexpr int BUDGET = 232448 - EPI - RAWB - 1024 - 512 - HS * HSLOT;
   // BRES (GS2D with CONCAT or TF32): the whole B (8 k-blocks, K = 256) stays resident -- stage kb holds
   // k-block kb for the kernel's lifetime; otherwise B streams through an S-stage ring per unit.
-  static constexpr bool BRES = GEOM == GS2D && (CONCAT || !THREE_X);
+  static constexpr bool BRES = Geo<GEOM>::RAWG && (CONCAT || !THREE_X || GEOM == G3C4);
   static constexpr int S = BRES ? Geo<GEOM>::KB_PER_UNIT : ((BUDGET / BSTAGE) > 12 ? 12 : (BUDGET / BSTAGE));
   static_assert(!BRES || S * BSTAGE <= BUDGET, "resident B does not fit");
   static constexpr int SMEM = HS * HSLOT + S * BSTAGE + EPI + RAWB + 1024 + 512;
   static constexpr int AS = ATM ? (512 - 2 * ACC) / 64 : 0;            // ATM: TMEM tap slots
   static constexpr uint32_t A_COL0 = 2 * ACC;                            // first column of the tap slots
-  static constexpr uint32_t TMEM_COLS = ATM ? 512 : 2 * ACC;
+  // accumulator buffers: G3C4 (short tiles) keeps four in TMEM so the epilogue of tile i overlaps the
+  // MMAs of tiles i+1 .. i+3; the others double-buffer
+  static constexpr int NACC = GEOM == G3C4 ? 4 : 2;
+  static constexpr uint32_t TMEM_COLS = ATM ? 512 : NACC * ACC;
   static_assert(S >= 2, "halo kernel needs >= 2 B stages");
   static_assert(!ATM || AS >= 2, "ATM needs >= 2 TMEM tap slots");
-  static_assert(2 * ACC <= 512, "TMEM");
+  static_assert(NACC * ACC <= 512, "TMEM");
 };
 
 struct HTile {
@@ -129,7 +157,7 @@ __device__ __forceinline__ HTile hdecode(const HArgs& a, int t, uint32_t rank) {
 }
 
 template <int BN, bool THREE_X, int GEOM>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
     halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmBh,
                 const __grid_constant__ CUtensorMap tmBhF, const __grid_constant__ CUtensorMap tmBlF,
                 const __grid_constant__ CUtensorMap tmD,
@@ -153,17 +181,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
   uint64_t* b_full = h_empty + HS;
   uint64_t* b_empty = b_full + S;
   uint64_t* tmem_full = b_empty + S;
-  uint64_t* tmem_empty = tmem_full + 2;
-  uint64_t* raw_ld = tmem_empty + 2;     // raw patch landed (TMA -> transform)
-  uint64_t* raw_empty = raw_ld + 1;      // raw patch consumed (transform -> producer)
-  uint64_t* a_full = raw_empty + 1;      // ATM: tap slot written (both CTAs' transform warps -> leader MMA)
+  uint64_t* tmem_empty = tmem_full + C_::NACC;
+  uint64_t* raw_ld = tmem_empty + C_::NACC;     // raw patch landed (TMA -> transform), per ring slot
+  uint64_t* raw_empty = raw_ld + 4;      // raw patch consumed (transform -> producer), per ring slot
+  uint64_t* a_full = raw_empty + 4;      // ATM: tap slot written (both CTAs' transform warps -> leader MMA)
   uint64_t* a_empty = a_full + 4;        // ATM: tap slot read by the MMAs (commit -> transform warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
-  const int KBU = GEOM == GS2D ? args.kbu : G_::KB_PER_UNIT;
+  const int KBU = G_::RAWG ? args.kbu : G_::KB_PER_UNIT;
   pdl_trigger();  // launch.cuh
   if (threadIdx.x == 0 && args.trace) args.trace[blockIdx.x * 8 + 0] = globaltimer_ns();
 
@@ -181,12 +209,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       mbar_init(&b_full[s], 1);
       mbar_init(&b_empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < C_::NACC; ++a) {
       mbar_init(&tmem_full[a], 1);
-      mbar_init(&tmem_empty[a], 2 * 128);
+      mbar_init(&tmem_empty[a], 2 * 32 * G_::EW);
     }
-    mbar_init(raw_ld, 1);
-    mbar_init(raw_empty, 128);
+    for (int r = 0; r < 4; ++r) {
+      mbar_init(&raw_ld[r], 1);
+      mbar_init(&raw_empty[r], 128);
+    }
     fence_mbar_init();
   }
   if (warp == 4 && lane == 0) {
@@ -217,14 +247,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const HTile tl = hdecode(args, cid + (u / args.ncb) * ncl, rank);
         const int cb = u % args.ncb;
         const int h = u % HS;
-        if (u >= HS) mbar_wait(&h_empty[h], ((u / HS) - 1) & 1);
-        if (GEOM == GS2D && args.raw) {  // raw patch; the transform warps write the halo slot
-          if (u >= 1) mbar_wait(raw_empty, (u - 1) & 1);
-          mbar_arrive_expect_tx(raw_ld, (uint32_t)(RAW_ROWS * raw_row_floats(args.rc) * 4));
-          const int col0 = (2 * tl.wo0 - args.rpl) * args.rc;
-          tma_load_3d(&tmX, raw_ld, smem_u32(raw), col0 - (col0 & 3), 2 * tl.ho0 - args.rpt, tl.n);
+        if (G_::RAWG && args.raw) {  // raw patch into ring slot u % NR; the transform warps write the halo slot
+          const int r = u % C_::NR;
+          if (u >= C_::NR) mbar_wait(&raw_empty[r], ((u / C_::NR) - 1) & 1);
+          mbar_arrive_expect_tx(&raw_ld[r], (uint32_t)(raw_rows<GEOM>() * raw_floats<GEOM>(args.rc) * 4));
+          const int sc = GEOM == GS2D ? 2 : 1;  // input pixels per output pixel
+          const int col0 = (sc * tl.wo0 - args.rpl) * args.rc;
+          tma_load_3d(&tmX, &raw_ld[r], smem_u32(raw + r * C_::RAW_SLOT), col0 - (col0 & 3), sc * tl.ho0 - args.rpt,
+                      tl.n);
           return;
         }
+        if (u >= HS) mbar_wait(&h_empty[h], ((u / HS) - 1) & 1);
         mbar_arrive_expect_tx(&h_ld[h], (uint32_t)(G_::HALO_ROWS * G_::ROWB));  // box bytes
         tma_load_4d(&tmX, &h_ld[h], smem_u32(halo_hi(h)), cb * BK, tl.wo0 - args.PL, tl.ho0 - args.PT, tl.n);
       };
@@ -235,6 +268,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           if (C_::CONCAT)
             tma_load_3d_2sm(rank == 0 ? (const void*)&tmBhF : (const void*)&tmBlF, b_full_leader, smem_u32(b_z(kb)),
                             kb * BK, 0, 0);
+          else if (THREE_X)  // G3C4, BN = 128: the B_lo half
+            tma_load_3d_2sm(&tmBlF, b_full_leader, smem_u32(b_lo(kb)), kb * BK, (int)rank * (BN / 2), 0);
         }
       }
       if (units > 0) issue_halo(0);
@@ -252,7 +287,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           const uint32_t fb = b_full_leader + (uint32_t)(s * sizeof(uint64_t));
           // filter prep order k = tap * C + c: G3X3 k-block kb = tap kb, channel block cb; GS2D k-block
           // kb = taps 2kb, 2kb+1 (16 channels each)
-          const int k0 = GEOM == GS2D ? kb * BK : (kb * args.ncb + cb) * BK;
+          const int k0 = G_::RAWG ? kb * BK : (kb * args.ncb + cb) * BK;
           tma_load_3d_2sm(&tmBh, fb, smem_u32(b_x(s)), k0, nrow, 0);
           if (C_::CONCAT)  // CTA0: B_hi rows [ni*BN, +BN); CTA1: B_lo rows [ni*BN, +BN)
             tma_load_3d_2sm(rank == 0 ? (const void*)&tmBhF : (const void*)&tmBlF, fb, smem_u32(b_z(s)), k0,
@@ -279,9 +314,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         tc_fence_after();
       }
       for (int t = cid; t < args.total; t += ncl, ++ai) {
-        const int acc = ai & 1;
-        uint64_t soff_next = GEOM == GS2D ? args.soff[0] : 0;  // GS2D: next k-block's view offsets, a step ahead
-        if (ai >= 2) mbar_wait(&tmem_empty[acc], ((ai >> 1) - 1) & 1);
+        const int acc = (int)(ai % C_::NACC);
+        uint64_t soff_next = G_::RAWG ? args.soff[0] : 0;  // GS2D / G3C4: next k-block's view offsets, a step ahead
+        if (ai >= (uint32_t)C_::NACC) mbar_wait(&tmem_empty[acc], ((ai / C_::NACC) - 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * C_::ACC);
         for (int cb = 0; cb < args.ncb; ++cb, ++hit) {
@@ -290,9 +325,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             mbar_wait(&h_full[h], (hit / HS) & 1);
             tc_fence_after();
           }
+          if constexpr (GEOM == G3C4) {  // B resident (stages 0, 1): the whole tile from one asm block
+            static_assert(C_::BRES, "G3C4 keeps B resident");
+            const uint64_t ah = umma_desc_interleave_kmajor(smem_u32(halo_hi(h)), 16u, HWD * G_::ROWB);
+            const uint64_t al = THREE_X ? umma_desc_interleave_kmajor(smem_u32(halo_lo(h)), 16u, HWD * G_::ROWB) : 0;
+            if (C_::CONCAT)
+              mma2_c4_tile_concat(d, ah, al, umma_desc_sw128_kmajor(smem_u32(b_z(0))),
+                                  umma_desc_sw128_kmajor(smem_u32(b_z(1))), umma_desc_sw128_kmajor(smem_u32(b_x(0))),
+                                  umma_desc_sw128_kmajor(smem_u32(b_x(1))), idesc2, idesc);
+            else if (THREE_X)
+              mma2_c4_tile_3x(d, ah, al, umma_desc_sw128_kmajor(smem_u32(b_x(0))),
+                              umma_desc_sw128_kmajor(smem_u32(b_x(1))), umma_desc_sw128_kmajor(smem_u32(b_lo(0))),
+                              umma_desc_sw128_kmajor(smem_u32(b_lo(1))), idesc);
+            else
+              mma2_c4_tile_1x(d, ah, umma_desc_sw128_kmajor(smem_u32(b_x(0))),
+                              umma_desc_sw128_kmajor(smem_u32(b_x(1))), idesc);
+            mma_commit_2sm_mc_warp(&h_empty[h], 0x3);
+            continue;
+          }
           for (int kb = 0; kb < KBU; ++kb, ++bit) {
             const uint64_t soff = soff_next;
-            if constexpr (GEOM == GS2D) soff_next = args.soff[kb + 1 < 8 ? kb + 1 : 7];
+            if constexpr (G_::RAWG) soff_next = args.soff[kb + 1 < 8 ? kb + 1 : 7];
             const int s = C_::BRES ? kb : (int)(bit % S);
             if (!C_::BRES) {
               mbar_wait(&b_full[s], (bit / S) & 1);
@@ -305,8 +358,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             auto view = [&](uint32_t base, int tap) {
               const int r = tap / G_::TAPW, c = tap % G_::TAPW;
               const uint32_t a = base + (uint32_t)((r * HWD + c) * G_::ROWB);
-              return GEOM == GS2D ? umma_desc_sw64_kmajor_sbo(a, HWD * G_::ROWB)
-                                  : umma_desc_sw128_kmajor_sbo(a, HWD * G_::ROWB, 0u);
+              return GEOM == GS2D   ? umma_desc_sw64_kmajor_sbo(a, HWD * G_::ROWB)
+                     : GEOM == G3C4 ? umma_desc_interleave_kmajor(a, 16u, HWD * G_::ROWB)  // LBO: next pixel
+                                    : umma_desc_sw128_kmajor_sbo(a, HWD * G_::ROWB, 0u);
             };
             if constexpr (C_::ATM) {  // A from the TMEM tap slot the transform warps filled
               const int slot = (int)(ait % C_::AS);
@@ -327,7 +381,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               ++ait;
               continue;
             }
-            const int tap0 = GEOM == GS2D ? 0 : kb;
+            const int tap0 = G_::RAWG ? 0 : kb;
             const uint64_t dah0 = view(smem_u32(halo_hi(h)), tap0);
             const uint64_t dal0 = THREE_X ? view(smem_u32(halo_lo(h)), tap0) : 0;
             const uint64_t dbx = umma_desc_sw128_kmajor(smem_u32(b_x(s)));
@@ -344,7 +398,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
               // A: G3X3 steps through the tap's 128-byte row; GS2D step 4kb+k is (tap, half) from the step
               // table: the tap's view plus 32 bytes for the second 8 slots (uniform arithmetic, no branch)
               uint64_t dah, dal;
-              if constexpr (GEOM == GS2D) {
+              if constexpr (G_::RAWG) {
                 const uint64_t off = (soff >> (16 * k)) & 0xFFFFu;
                 dah = dah0 + off;
                 dal = dal0 + off;
@@ -417,11 +471,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
           mbar_arrive(&h_empty[h]);  // every tap of this halo is in TMEM: the producer may refill the slot
           continue;
         }
+        if (GEOM == G3C4 && args.raw) {
+          // build the 4-channel halo: pixel p = (hr, wc) of the 18 x 16 halo is one 16-byte row, slot
+          // c <- raw[hr][wc][c] for c < C, zero past C (and for the columns wc > 10 no view reaches)
+          const int rs = (int)(hit % C_::NR);
+          mbar_wait(&raw_ld[rs], (hit / C_::NR) & 1);
+          if (hit >= (uint32_t)HS) mbar_wait(&h_empty[h], ((hit / HS) - 1) & 1);  // the MMAs released the slot
+          const HTile tl = hdecode(args, tt, rank);
+          const int C = args.rc, rowf = raw_row_floats_c4(C);
+          const int shift = ((tl.wo0 - args.rpl) * C) & 3;  // patch origin within the aligned load
+          const uint32_t rb = smem_u32(raw + rs * C_::RAW_SLOT), hh = smem_u32(halo_hi(h)), hl = smem_u32(halo_lo(h));
+          const int wc = t & (HWD - 1);  // fixed per thread: p advances by 128 = 8 halo rows
+          int soff[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) soff[e] = (e < C && wc <= 10) ? shift + wc * C + e : -1;
+          for (int p = t; p < G_::HALO_ROWS; p += 128) {
+            const uint32_t rrow = rb + 4u * (uint32_t)((p / HWD) * rowf);
+            float v[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) v[e] = soff[e] >= 0 ? lds32(rrow + 4u * (uint32_t)soff[e]) : 0.f;
+            sts128(hh + (uint32_t)(p * 16), make_float4(v[0], v[1], v[2], v[3]));
+            if (THREE_X)
+              sts128(hl + (uint32_t)(p * 16), make_float4(v[0] - tf32_hi(v[0]), v[1] - tf32_hi(v[1]),
+                                                          v[2] - tf32_hi(v[2]), v[3] - tf32_hi(v[3])));
+          }
+          mbar_arrive(&raw_empty[rs]);
+          fence_proxy_async_smem();
+          mbar_arrive_remote(h_full_leader + (uint32_t)(h * sizeof(uint64_t)));
+          continue;
+        }
         if (GEOM == GS2D && args.raw) {
           // build the s2d halo: pixel p = (hi, wi) of the 19 x 16 halo, 16-byte chunk k = slots 4k..4k+3,
           // slot = (b*2 + d)*C + c <- raw[2*hi + b][2*wi + d][c]; SWIZZLE_64B placement (chunk k of the
           // 64-byte pixel row goes to k ^ ((p >> 1) & 3)), as the TMA would have written X'
           mbar_wait(raw_ld, hit & 1);
+          if (hit >= (uint32_t)HS) mbar_wait(&h_empty[h], ((hit / HS) - 1) & 1);  // the MMAs released the slot
           const HTile tl = hdecode(args, tt, rank);
           const int C = args.rc, rowf = raw_row_floats(C);
           const int shift = ((2 * tl.wo0 - args.rpl) * C) & 3;  // patch origin within the aligned load
@@ -470,24 +554,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
       }
     }
   } else {
-    // ============================ epilogue (warps 6-9) ============================
-    // warp q owns TMEM lanes [32q, 32q+32) = output rows ho0 + 4q .. +3, wo0 .. wo0+7
+    // ============================ epilogue (warps 6 .. 6 + EW) ============================
+    // warp q = warp % 4 owns TMEM lanes [32q, 32q+32) = output rows ho0 + 4q .. +3, wo0 .. wo0+7; with
+    // EW = 8 the two warps of a quarter take alternate 32-column chunks
     const int q = warp & 3;
+    constexpr int CSTEP = 32 * (G_::EW / 4);
+    const int cfirst = 32 * ((warp - 6) / 4);
     const uint32_t tmem_empty_leader = mapa(smem_u32(tmem_empty), 0);
-    const uint32_t ebuf = smem_u32(epi_smem) + (uint32_t)(q * 2 * 4096);
+    const uint32_t ebuf = smem_u32(epi_smem) + (uint32_t)((warp - 6) * 2 * 4096);
     if (args.tma_store && lane == 0) tma_prefetch(&tmD);
     uint32_t ai = 0, chunk = 0;
     for (int t = cid; t < args.total; t += ncl, ++ai) {
       const HTile tl = hdecode(args, t, rank);
-      const int acc = ai & 1;
-      mbar_wait(&tmem_full[acc], (ai >> 1) & 1);
+      const int acc = (int)(ai % C_::NACC);
+      mbar_wait(&tmem_full[acc], (ai / C_::NACC) & 1);
       tc_fence_after();
       const int ho = tl.ho0 + 4 * q + lane / 8, wo = tl.wo0 + lane % 8;
       const bool row_ok = tl.n < args.N && ho < args.HO && wo < args.WO;
       const bool warp_ok = tl.n < args.N && tl.ho0 + 4 * q < args.HO;
       const int n0 = tl.ni * BN;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = cfirst; c0 < BN; c0 += CSTEP) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C_::ACC + c0), v);
         if (C_::CONCAT) {  // add the hi*B_lo correction columns
@@ -496,7 +583,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int k = 0; k < 32; ++k) v[k] += w[k];
         }
-        if (c0 + 32 >= BN) {
+        if (c0 + CSTEP >= BN) {
           tc_fence_before();
           mbar_arrive_remote(tmem_empty_leader + (uint32_t)(acc * sizeof(uint64_t)));
         }
@@ -544,7 +631,7 @@ cudaError_t launch_h(const CUtensorMap& x, const CUtensorMap& bh, const CUtensor
   auto kern = halo_kernel<BN, THREE_X, GEOM>;
   const cudaError_t e = smem_attr_once<halo_kernel<BN, THREE_X, GEOM>>(C_::SMEM);
   if (e != cudaSuccess) return e;
-  return launch_k(kern, dim3(2 * clusters), dim3(NTHREADS), C_::SMEM, s, x, bh, bhf, blf, dm, a);
+  return launch_k(kern, dim3(2 * clusters), dim3(Geo<GEOM>::NT), C_::SMEM, s, x, bh, bhf, blf, dm, a);
 }
 
 }  // namespace
@@ -600,14 +687,18 @@ cudaError_t launch_halo_geo(const Problem& p, const float* x, int h, int w, int 
   a.ldd = p.F;
   a.d = out;
   alignas(64) CUtensorMap tx{}, tbh{}, tbhf{}, tblf{}, td{};
-  if (raw) {  // GS2D raw mode: patches {32 * C floats, RAW_ROWS rows, 1} of x viewed as (N, H, W*C)
+  if (GEOM == G3C4) {  // six steps (r, q): taps (r, 2q) and (r, 2q + 1); steps 6, 7 have zero B rows
+    for (int i = 0; i < 6; ++i) a.soff[i / 4] |= (uint64_t)((i / 2) * HWD + 2 * (i % 2)) << (16 * (i % 4));
+    a.kbu = 2;
+  }
+  if (raw) {  // raw mode: patches {raw floats, raw rows, 1} of x viewed as (N, H, W*C)
     a.raw = 1;
     a.rc = p.C;
     a.rpt = p.pad_top;
     a.rpl = p.pad_left;
     const uint64_t dims[3] = {(uint64_t)p.W * p.C, (uint64_t)p.H, (uint64_t)p.N};
     const uint64_t st[2] = {(uint64_t)p.W * p.C * 4, (uint64_t)p.H * p.W * p.C * 4};
-    const uint32_t box[3] = {(uint32_t)raw_row_floats(p.C), (uint32_t)RAW_ROWS, 1};
+    const uint32_t box[3] = {(uint32_t)raw_floats<GEOM>(p.C), (uint32_t)raw_rows<GEOM>(), 1};
     if (!gemm2_encode_tiled(&tx, 3, x, dims, st, box, false)) return cudaErrorInvalidValue;
   } else {  // input halo boxes {32 | 16 ch, 16 w, HHT h, 1 n} over NHWC, OOB (padding) -> 0
     const uint64_t dims[4] = {(uint64_t)cx, (uint64_t)w, (uint64_t)h, (uint64_t)p.N};
@@ -704,12 +795,58 @@ __global__ void s2d_filter_kernel(const float* __restrict__ w, int KH, int KW, i
     if (bt_lo) bt_lo[i] = v - h;
   }
 }
+// Bt[f][k] (npad x 64, K-major) for G3C4: k = 8 * step + j, step (r, q) = (step / 2, step % 2) < 6,
+// tap s = 2q + j / 4, channel c = j % 4  <-  w[r][s][c][f] (zero for s = 3, c >= C, f >= F, steps 6, 7)
+__global__ void c4_filter_kernel(const float* __restrict__ w, int C, int F, int64_t npad, float* __restrict__ bt_hi,
+                                 float* __restrict__ bt_lo) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t total = npad * 64;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % 64);
+    const int f = (int)(i / 64);
+    const int step = k / 8, j = k % 8;
+    const int r = step / 2, sc = 2 * (step % 2) + j / 4, c = j % 4;
+    float v = 0.f;
+    if (step < 6 && sc < 3 && c < C && f < F) v = w[((int64_t)(r * 3 + sc) * C + c) * F + f];
+    const float h = bt_lo ? tf32_hi(v) : v;
+    bt_hi[i] = h;
+    if (bt_lo) bt_lo[i] = v - h;
+  }
+}
 }  // namespace
 
 cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_hi, const float* bt_lo, int64_t kpad,
                              int64_t npad, int block_n, float* out, cudaStream_t s) {
   return launch_halo_geo<G3X3>(p, in, p.H, p.W, p.C, p.pad_top, p.pad_left, p.C / 32, bt_hi, bt_lo, kpad, npad,
                                block_n, out, s);
+}
+
+// G3C4: 3x3 / stride 1 with C <= 4, raw patches straight from x (16-byte rows of W*C floats)
+bool c4_ok(const Problem& p) {
+  return p.KH == 3 && p.KW == 3 && p.SH == 1 && p.SW == 1 && p.C <= 4 && p.F <= 128 &&
+         ((int64_t)p.W * p.C) % 4 == 0 && (int64_t)p.W * p.C < (1LL << 31) &&
+         (int64_t)p.N * ((p.HO + TH - 1) / TH) * ((p.WO + TW - 1) / TW) < (1 << 30);
+}
+
+size_t c4_workspace(const Problem& p, int block_n, bool three_x) {
+  const int64_t npad = (p.F + block_n - 1) / block_n * block_n;
+  const size_t bt = (size_t)((npad * 64 * 4 + 255) / 256 * 256);
+  return bt * (three_x ? 2 : 1);
+}
+
+cudaError_t launch_gemm_c4(const Problem& p, const float* in, const float* filt, int block_n, bool three_x, void* ws,
+                           float* out, cudaStream_t s) {
+  const int64_t npad = (p.F + block_n - 1) / block_n * block_n;
+  const size_t bt = (size_t)((npad * 64 * 4 + 255) / 256 * 256);
+  float* bt_hi = static_cast<float*>(ws);
+  float* bt_lo = three_x ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + bt) : nullptr;
+  const int64_t fb = (npad * 64 + 255) / 256;
+  const cudaError_t e =
+      launch_k(c4_filter_kernel, dim3((unsigned)fb), dim3(256), 0, s, filt, p.C, p.F, npad, bt_hi, bt_lo);
+  if (e != cudaSuccess) return e;
+  return launch_halo_geo<G3C4>(p, in, p.H, p.W, 4, p.pad_top, p.pad_left, 1, bt_hi, bt_lo, 64, npad, block_n, out, s,
+                               true);
 }
 
 size_t s2d_workspace(const Problem& p, int block_n, bool three_x) {

@@ -70,6 +70,9 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
   } else if (!is_1x1 && s2d_ok(p) && !(variant & 1) && getenv("CONV2D_NO_S2D") == nullptr) {
     pl.a_mode = A_S2D;  // 7x7/8x8 stride-2 stems, C <= 4: space-to-depth + 4x4 halo views (gemm_halo.cu)
     pl.cstride = p.C;
+  } else if (!is_1x1 && c4_ok(p) && !(variant & 1) && getenv("CONV2D_NO_C4") == nullptr) {
+    pl.a_mode = A_C4;  // 3x3 s1, C <= 4 (VGG conv1_1): 4-channel halo, two taps per K=8 step (gemm_halo.cu)
+    pl.cstride = p.C;
   } else if (!is_1x1 && halo_ok(p) && !(variant & 1) && getenv("CONV2D_NO_HALO") == nullptr) {
     pl.a_mode = A_HALO;  // 3x3 s1, small N: halo-tile reuse (gemm_halo.cu)
     pl.cstride = p.C;
@@ -79,8 +82,11 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
   } else if (gemm2_rowseg_ok(p)) {
     // small C, narrow windows (the C=3 stems): A_ROWSEG (one overlapping-stride TMA box per kernel
     // row) by default, A_STEM (halo + transform-built rows) as the tunable alternative
-    // (for s2d-eligible stems bit 0 selects this path over A_S2D)
-    pl.a_mode = ((variant & 1) && !s2d_ok(p) && gemm2_stem_ok(p, pl.block_n, pl.three_x)) ? A_STEM : A_ROWSEG;
+    // (for s2d- and c4-eligible layers bit 0 selects this path over A_S2D / A_C4)
+    pl.a_mode = ((variant & 1) && !s2d_ok(p) && !(c4_ok(p) && getenv("CONV2D_NO_C4") == nullptr) &&
+                 gemm2_stem_ok(p, pl.block_n, pl.three_x))
+                    ? A_STEM
+                    : A_ROWSEG;
     pl.cg = (int)round_up(p.C, 4);
     pl.pad = true;         // spatial + channel padding pass
     pl.cstride = pl.cg;
@@ -114,6 +120,15 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
     pl.splits = 1;
     pl.b_mn = false;
     pl.total = s2d_workspace(p, pl.block_n, pl.three_x);
+    return pl;
+  }
+  if (pl.a_mode == A_C4) {
+    if (pl.block_n == 256) pl.block_n = 128;
+    pl.kpad = 64;
+    pl.npad = round_up(p.F, pl.block_n);
+    pl.splits = 1;
+    pl.b_mn = false;
+    pl.total = c4_workspace(p, pl.block_n, pl.three_x);
     return pl;
   }
   const bool rowk = pl.a_mode == A_ROWSEG || pl.a_mode == A_STEM;  // k = (kernel row, 32 floats)
@@ -153,6 +168,7 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
 int igemm_variants(const Problem& p, bool is_1x1, int* masks) {
   const bool alt_a = is_1x1 ? (p.C % 4 == 0 && p.C >= 32 && gemm2_im2col_ok(p))
                             : ((halo_ok(p) && gemm2_im2col_ok(p)) || (s2d_ok(p) && gemm2_rowseg_ok(p)) ||
+                               (c4_ok(p) && gemm2_rowseg_ok(p)) ||
                                (gemm2_rowseg_ok(p) && gemm2_stem_ok(p, gemm2_choose_block_n(p.F), p.math == 0)));
   const bool alt_n = gemm2_choose_block_n(p.F) == 256;
   // bit 3 matters only where some A path reads B directly (im2col / dense, F % 32 == 0) in 3xTF32 mode
@@ -207,12 +223,13 @@ size_t igemm_workspace(const Problem& p, bool is_1x1) {
 int igemm_launches(const Problem& p, bool is_1x1) {
   const Plan pl = make_plan(p, is_1x1, variant_of(p, is_1x1));
   if (pl.a_mode == A_S2D) return (p.C <= 3 && ((int64_t)p.W * p.C) % 4 == 0) ? 2 : 3;  // [s2d input,] filter, GEMM
+  if (pl.a_mode == A_C4) return 2;                                                      // filter, GEMM
   return (pl.b_mn ? 1 : 2) + (pl.pad ? 1 : 0) + (pl.splits > 1 || pl.rsplit ? 1 : 0);
 }
 
 int igemm_split_desc(const Problem& p, bool is_1x1) {
   const Plan pl = make_plan(p, is_1x1, variant_of(p, is_1x1));
-  if (pl.a_mode == A_S2D) return 1;
+  if (pl.a_mode == A_S2D || pl.a_mode == A_C4) return 1;
   return pl.rsplit ? -gemm2_rsplit_factor(((p.M() + 255) / 256) * ((p.F + pl.block_n - 1) / pl.block_n),
                                           (int)(pl.kpad / 32))
                    : pl.splits;
@@ -223,6 +240,7 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
   const Plan pl = make_plan(p, is_1x1, variant_of(p, is_1x1));
   static const bool debug = getenv("CONV2D_DEBUG") != nullptr;
   if (pl.a_mode == A_S2D) return launch_gemm_s2d(p, in, filt, pl.block_n, pl.three_x, ws, out, s);
+  if (pl.a_mode == A_C4) return launch_gemm_c4(p, in, filt, pl.block_n, pl.three_x, ws, out, s);
   if (debug)
     fprintf(stderr, "[conv2d] igemm N=%d H=%d W=%d C=%d F=%d K=%dx%d S=%d: a_mode=%d bn=%d splits=%d kpad=%lld 3x=%d\n",
             p.N, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH, pl.a_mode, pl.block_n, pl.splits, (long long)pl.kpad,

@@ -624,3 +624,102 @@ __device__ __forceinline__ void mma2_kblock_tt_3x(uint32_t d, uint32_t ahi_tmem,
       : "memory");
 }
 }  // namespace sm100
+
+namespace sm100 {
+// halo kernel G3C4 (gemm_halo.cu): a whole tile's six K=8 steps from one asm block (one elect).  Step i
+// reads the A view at halo offset {0, 2, 16, 18, 32, 34}[i] (16-byte units: tap row r = i / 2, tap pair
+// q = i % 2) and B k-block i / 4 (resident stages: descriptors *0 / *1) at 32 * (i % 4) bytes.  The first
+// MMA overwrites the accumulator.
+__device__ __forceinline__ void mma2_c4_tile_concat(uint32_t d, uint64_t ah, uint64_t al, uint64_t bz0, uint64_t bz1, uint64_t bx0, uint64_t bx1, uint32_t idesc2,
+    uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a, b, c;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, 0, 0;\n\tsetp.eq.u32 t, 0, 0;\n\t"
+      "add.u64 a, %1, 0;\n\tadd.u64 b, %3, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, p;\n\t"
+      "add.u64 a, %2, 0;\n\tadd.u64 c, %5, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, c, %8, t;\n\t"
+      "add.u64 a, %1, 2;\n\tadd.u64 b, %3, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %2, 2;\n\tadd.u64 c, %5, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, c, %8, t;\n\t"
+      "add.u64 a, %1, 16;\n\tadd.u64 b, %3, 4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %2, 16;\n\tadd.u64 c, %5, 4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, c, %8, t;\n\t"
+      "add.u64 a, %1, 18;\n\tadd.u64 b, %3, 6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %2, 18;\n\tadd.u64 c, %5, 6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, c, %8, t;\n\t"
+      "add.u64 a, %1, 32;\n\tadd.u64 b, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %2, 32;\n\tadd.u64 c, %6, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, c, %8, t;\n\t"
+      "add.u64 a, %1, 34;\n\tadd.u64 b, %4, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %2, 34;\n\tadd.u64 c, %6, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, c, %8, t;\n\t"
+      "}" ::"r"(d), "l"(ah), "l"(al), "l"(bz0), "l"(bz1), "l"(bx0), "l"(bx1), "r"(idesc2), "r"(idesc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_c4_tile_3x(uint32_t d, uint64_t ah, uint64_t al, uint64_t bx0, uint64_t bx1, uint64_t bl0, uint64_t bl1,
+    uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a, b, c;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, 0, 0;\n\tsetp.eq.u32 t, 0, 0;\n\t"
+      "add.u64 a, %2, 0;\n\tadd.u64 b, %3, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, p;\n\t"
+      "add.u64 a, %1, 0;\n\tadd.u64 c, %5, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, c, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %2, 2;\n\tadd.u64 b, %3, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %1, 2;\n\tadd.u64 c, %5, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, c, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %2, 16;\n\tadd.u64 b, %3, 4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %1, 16;\n\tadd.u64 c, %5, 4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, c, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %2, 18;\n\tadd.u64 b, %3, 6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %1, 18;\n\tadd.u64 c, %5, 6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, c, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %2, 32;\n\tadd.u64 b, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %1, 32;\n\tadd.u64 c, %6, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, c, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %2, 34;\n\tadd.u64 b, %4, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "add.u64 a, %1, 34;\n\tadd.u64 c, %6, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, c, %7, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %7, t;\n\t"
+      "}" ::"r"(d), "l"(ah), "l"(al), "l"(bx0), "l"(bx1), "l"(bl0), "l"(bl1), "r"(idesc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_c4_tile_1x(uint32_t d, uint64_t ah, uint64_t bx0, uint64_t bx1, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a, b;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, 0, 0;\n\tsetp.eq.u32 t, 0, 0;\n\t"
+      "add.u64 a, %1, 0;\n\tadd.u64 b, %2, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %4, p;\n\t"
+      "add.u64 a, %1, 2;\n\tadd.u64 b, %2, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %4, t;\n\t"
+      "add.u64 a, %1, 16;\n\tadd.u64 b, %2, 4;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %4, t;\n\t"
+      "add.u64 a, %1, 18;\n\tadd.u64 b, %2, 6;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %4, t;\n\t"
+      "add.u64 a, %1, 32;\n\tadd.u64 b, %3, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %4, t;\n\t"
+      "add.u64 a, %1, 34;\n\tadd.u64 b, %3, 2;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], a, b, %4, t;\n\t"
+      "}" ::"r"(d), "l"(ah), "l"(bx0), "l"(bx1), "r"(idesc)
+      : "memory");
+}
+}  // namespace sm100

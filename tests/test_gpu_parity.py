@@ -394,6 +394,37 @@ def test_algorithm_parameter_variants(cuda_ok, monkeypatch, variant, case):
             assert_int_exact(p, gpu_conv(p, xi, wi, a), refi, deni, a, f"variant int {case} {a}")
 
 
+C4_CASES = [  # (N, H, W, C, F, KH, KW, SH, SW, pad): 3x3 / s1, C <= 4, W*C % 4 == 0 (raw 16-byte rows)
+    (1, 224, 224, 3, 64, 3, 3, 1, 1, 0),   # VGG conv1_1 at batch 1 (the north_star small layer)
+    (2, 20, 24, 3, 64, 3, 3, 1, 1, 0),     # ragged 16-row tiles, 3 column tiles
+    (3, 17, 12, 1, 17, 3, 3, 1, 1, 1),     # VALID, C = 1, F % 4 != 0 (LSU epilogue), odd tile count
+    (1, 9, 6, 2, 40, 3, 3, 1, 1, 0),       # C = 2, one tile
+    (2, 33, 29, 4, 128, 3, 3, 1, 1, 0),    # C = 4 (no zero slots), BN = 128
+    (1, 40, 36, 3, 200, 3, 3, 1, 1, 1),    # F > 128: two N tiles
+]
+
+
+@pytest.mark.parametrize("case", C4_CASES, ids=str)
+def test_igemm_c4_halo(cuda_ok, monkeypatch, case):
+    """implicit_gemm's A_C4 path (gemm_halo.cu G3C4: 3x3 / s1 with C <= 4, two taps per K=8 MMA step
+    through overlapping 16-byte-pixel views) against the oracle: integer-exact and within tolerance,
+    both math modes; bit 0 (the row-segment path) agrees with it."""
+    p0 = P(*case)
+    x, w = make_inputs(p0, layer_id=960)
+    ref, den = O.conv2d(oparams(p0), x, w, with_denom=True)
+    xi, wi = make_inputs(p0, layer_id=961, dist=synth.DIST_INT5)
+    refi, deni = O.conv2d(oparams(p0), xi, wi, with_denom=True)
+    a = C().ALGO_IMPLICIT_GEMM
+    for variant in (0, 1):
+        monkeypatch.setenv("CONV2D_FORCE_VARIANT", str(variant))
+        for math in MATHS:
+            p = p0.replace(math=math)
+            if variant == 0 and p0.features <= 128:
+                assert C().conv2d_launch_count(p, a) == 2  # B prep + the halo GEMM, no padding pass
+            check_close(p, gpu_conv(p, x, w, a), ref, den, a, f"c4 v{variant} {case} math={math}")
+            assert_int_exact(p, gpu_conv(p, xi, wi, a), refi, deni, a, f"c4 int v{variant} {case} math={math}")
+
+
 WINO_FUSED_CASES = [l.params(1) for l in ALL_SHAPES if l.window == 3 and l.stride == 1 and l.channels >= 32] + [
     dict(batch=3, in_rows=15, in_cols=9, channels=64, features=68, window_rows=3, window_cols=3, stride_rows=1,
          stride_cols=1, padding=1),    # VALID, ragged tile blocks, F % 32 != 0
