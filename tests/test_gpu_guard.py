@@ -38,6 +38,8 @@ SHAPES = [
     (3, 11, 12, 8, 16, 4, 4, 2, 1, 0),
     (1, 13, 11, 5, 130, 3, 3, 2, 1, 0),
     (2, 33, 70, 3, 64, 3, 3, 1, 1, 0),       # V1-like small C for the tiled kernel's vector paths
+    (2, 33, 68, 3, 64, 3, 3, 1, 1, 0),       # implicit_gemm A_C4 (4-channel halo; W*C % 4 == 0), ragged tiles
+    (3, 17, 12, 1, 17, 3, 3, 1, 1, 1),       # A_C4, C = 1, VALID, F % 4 != 0 (LSU epilogue)
     (1, 9, 9, 20, 24, 5, 5, 1, 1, 0),        # tiled generic (runtime KW) path, F % 16 != 0
     # fused Winograd F(2x2) (winograd_f2x2_3x3 variant 1): ragged tile blocks / NB > 1 / odd Ho, F % 32 != 0
     (3, 15, 9, 64, 68, 3, 3, 1, 1, 1),

@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--layers", default="R3,R12,R26")
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--math", choices=["fp32", "tf32"], default="fp32")
+    ap.add_argument("--flush", choices=["dirty", "clean", "none"], default="dirty",
+                    help="before the traced call: write 256 MiB (L2 full of dirty lines, as after a previous "
+                         "conv's output), read 256 MiB (clean lines), or nothing (inputs hot in L2)")
     args = ap.parse_args()
 
     import torch
@@ -53,7 +56,10 @@ def main():
         algo = C.ALGO_NAMES[C.conv2d_selected(p)]
         torch.cuda.synchronize()
         C.conv2d_debug_trace(1)
-        flush.zero_()
+        if args.flush == "dirty":
+            flush.zero_()
+        elif args.flush == "clean":
+            flush.max()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         C.conv2d_forward(p, C.ALGO_AUTO, x, w, y, ws, ws.numel(), stream)

@@ -23,7 +23,7 @@ from paper_1904_04174_b200 import synth  # noqa: E402
 
 # (N, H, W, C, F, KH, KW, SH, SW, pad): each reaches a different A-operand path / kernel
 SHAPES = [
-    (1, 8, 8, 4, 8, 3, 3, 1, 1, 0),          # config 1: direct, tiled, gather
+    (1, 8, 8, 4, 8, 3, 3, 1, 1, 0),          # config 1: direct, tiled, A_C4 (row-segment alternative)
     (2, 20, 20, 64, 64, 3, 3, 1, 1, 0),      # halo (F <= 128), im2col alternative, Winograd F2/F4
     (1, 14, 14, 128, 256, 3, 3, 1, 1, 1),    # im2col BN=256 / 128, Winograd VALID
     (2, 12, 12, 64, 256, 1, 1, 1, 1, 0),     # dense 1x1 (matmul_1x1), direct-B and K-major B
@@ -35,6 +35,8 @@ SHAPES = [
     (1, 44, 43, 48, 100, 1, 1, 1, 1, 0),     # gather A path with 3xTF32 lo in TMEM
     (3, 11, 12, 8, 16, 4, 4, 2, 1, 0),       # narrow im2col boxes
     (1, 13, 11, 5, 130, 3, 3, 2, 1, 0),      # C % 4 != 0: channel padding + gather
+    (2, 33, 68, 3, 64, 3, 3, 1, 1, 0),       # 4-channel halo (A_C4), row-segment alternative
+    (3, 17, 12, 1, 17, 3, 3, 1, 1, 1),       # A_C4 with C = 1, VALID, F % 4 != 0
 ]
 QUICK = SHAPES[:4]
 
