@@ -25,6 +25,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=2000)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--focus", choices=["all", "c4"], default="all",
+                    help="c4: only 3x3 / stride 1 with C <= 4 (implicit_gemm's A_C4 4-channel halo path)")
     args = ap.parse_args()
 
     import torch
@@ -44,6 +46,13 @@ def main():
         w = int(rng.integers(max(kw, 1), 72))
         c = int(rng.choice([1, 2, 3, 4, 5, 8, 16, 24, 32, 48, 64, 96, 128, 256]))
         f = int(rng.choice([1, 3, 8, 16, 32, 33, 64, 96, 100, 128, 160, 256, 288, 512]))
+        if args.focus == "c4":
+            k = kw = 3
+            s = 1
+            c = int(rng.choice([1, 2, 3, 4]))
+            w = int(rng.integers(1, 40)) * (4 // np.gcd(c, 4))  # W*C % 4 == 0 (raw 16-byte rows)
+            h = int(rng.integers(1, 72))
+            f = int(rng.choice([1, 3, 8, 17, 32, 36, 64, 96, 100, 128]))
         pad = int(rng.integers(0, 2))
         math = int(rng.integers(0, 2))
         integer = rng.random() < 0.3
