@@ -77,6 +77,11 @@ struct HArgs {
   // per k-block kb: the four steps' A-view offsets from the halo base, in 16-byte descriptor units (u16 x 4)
   uint64_t soff[8];
   int kbu;
+  // G3C4: the transform warps build the resident B stages straight from the HWCF filter at kernel start
+  // (no filter-prep launch, no workspace); wc / wf = the filter's C and F
+  const float* w;
+  int wc, wf;
+  int wbulk;  // 1: the producer bulk-copies the filter (16-byte aligned, 9 C F % 4 == 0) in one cp.async.bulk
 };
 
 struct S2DSteps {
@@ -118,6 +123,7 @@ struct HCfg {
   static constexpr int BSTAGE = CONCAT ? BFULL + BHALF : (THREE_X ? 2 : 1) * BHALF;
   static constexpr int ACC = CONCAT ? 2 * BN : BN;                     // TMEM columns per accumulator
   static constexpr int EPI = Geo<GEOM>::EW * 2 * 32 * 128;
+  static_assert(GEOM != G3C4 || EPI >= 9 * 4 * 128 * 4, "G3C4 stages the filter in the epilogue buffers");
   static constexpr int RAWB = Geo<GEOM>::RAWG ? RAW_BYTES_MAX : 0;      // raw-patch staging
   // raw-patch ring: G3C4 patches are small (18 rows x 48 floats at most), so four are in flight -- a single
   // slot serialises every tile behind one TMA round trip (measured: 1.6 us per tile on VGG conv1_1)
@@ -186,7 +192,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
   uint64_t* raw_empty = raw_ld + 4;      // raw patch consumed (transform -> producer), per ring slot
   uint64_t* a_full = raw_empty + 4;      // ATM: tap slot written (both CTAs' transform warps -> leader MMA)
   uint64_t* a_empty = a_full + 4;        // ATM: tap slot read by the MMAs (commit -> transform warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_empty + 4);
+  uint64_t* w_ld = a_empty + 4;         // G3C4: the filter's bulk copy into the epilogue buffers landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_ld + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -206,7 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
       mbar_init(&a_empty[i], 1);
     }
     for (int s = 0; s < S; ++s) {
-      mbar_init(&b_full[s], 1);
+      mbar_init(&b_full[s], GEOM == G3C4 ? 2 * 32 * G_::EW : 1);  // G3C4: both CTAs' epilogue threads build B
       mbar_init(&b_empty[s], 1);
     }
     for (int a = 0; a < C_::NACC; ++a) {
@@ -215,6 +222,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
     }
     for (int r = 0; r < 4; ++r) {
       mbar_init(&raw_ld[r], 1);
+      if (r == 0) mbar_init(w_ld, 1);
       mbar_init(&raw_empty[r], 128);
     }
     fence_mbar_init();
@@ -261,7 +269,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
         mbar_arrive_expect_tx(&h_ld[h], (uint32_t)(G_::HALO_ROWS * G_::ROWB));  // box bytes
         tma_load_4d(&tmX, &h_ld[h], smem_u32(halo_hi(h)), cb * BK, tl.wo0 - args.PL, tl.ho0 - args.PT, tl.n);
       };
-      if (C_::BRES && units > 0) {  // all of B once (single N tile: F <= BN), to the leader's b_full[0]
+      if (C_::BRES && GEOM != G3C4 && units > 0) {  // all of B once (single N tile: F <= BN), to the leader's b_full[0]
         if (rank == 0) mbar_arrive_expect_tx(&b_full[0], 2 * KBU * C_::BSTAGE);
         for (int kb = 0; kb < KBU; ++kb) {
           tma_load_3d_2sm(&tmBh, b_full_leader, smem_u32(b_x(kb)), kb * BK, (int)rank * (BN / 2), 0);
@@ -271,6 +279,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
           else if (THREE_X)  // G3C4, BN = 128: the B_lo half
             tma_load_3d_2sm(&tmBlF, b_full_leader, smem_u32(b_lo(kb)), kb * BK, (int)rank * (BN / 2), 0);
         }
+      }
+      if (GEOM == G3C4 && args.wbulk && units > 0) {  // the filter, in flight with the first raw patches
+        const uint32_t bytes = (uint32_t)(9 * args.wc * args.wf * 4);
+        mbar_arrive_expect_tx(w_ld, bytes);
+        bulk_load(smem_u32(epi_smem), args.w, bytes, w_ld);
       }
       if (units > 0) issue_halo(0);
       uint32_t bit = 0;
@@ -563,6 +576,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
     const uint32_t tmem_empty_leader = mapa(smem_u32(tmem_empty), 0);
     const uint32_t ebuf = smem_u32(epi_smem) + (uint32_t)((warp - 6) * 2 * 4096);
     if (args.tma_store && lane == 0) tma_prefetch(&tmD);
+    if constexpr (GEOM == G3C4) {
+      const int et = (int)threadIdx.x - 6 * 32;
+      // resident B, K-major SWIZZLE_128B (row n: 128 bytes = k-block kb's 32 k; 16-byte chunk j at j ^ (n & 7)),
+      // k = 8 * step + j: step (r, q) = (step / 2, step % 2) < 6, tap s = 2q + j / 4, channel c = j % 4.
+      // CONCAT: b_z = B_hi (CTA0) / B_lo (CTA1), all BN rows; b_x = B_hi, this CTA's BN/2 rows.
+      // !CONCAT: b_x = B_hi [+ b_lo = B_lo], this CTA's BN/2 rows.  TF32: b_x = raw B.
+      // built by the epilogue warps, idle until the first accumulator (which needs this B) while the transform
+      // warps turn the first raw patches into halos; the filter (9 C F <= 4608 floats) is first staged in
+      // the epilogue's own smem: coalesced loads, all in flight together
+      float* wsm = reinterpret_cast<float*>(epi_smem);
+      const int nw = 9 * args.wc * args.wf;
+      const bool has_units = args.total > cid;
+      if (args.wbulk && has_units) {
+        mbar_wait(w_ld, 0);
+      } else {
+#pragma unroll 8
+        for (int i = et; i < nw; i += 256) wsm[i] = __ldg(args.w + i);
+        named_bar_sync(1, 256);
+      }
+      auto bval = [&](int f, int k, bool lo) {
+        const int step = k >> 3, j = k & 7, r = step >> 1, sc = 2 * (step & 1) + (j >> 2), c = j & 3;
+        float v = 0.f;
+        if (step < 6 && sc < 3 && c < args.wc && f < args.wf) v = wsm[((r * 3 + sc) * args.wc + c) * args.wf + f];
+        if (!THREE_X) return v;
+        const float hi = tf32_hi(v);
+        return lo ? v - hi : hi;
+      };
+      auto put = [&](uint8_t* base, int n, int k, float v) {
+        sts32(smem_u32(base) + (uint32_t)(n * 128 + ((((k & 31) >> 2) ^ (n & 7)) << 4) + (k & 3) * 4), v);
+      };
+      for (int kb = 0; kb < 2; ++kb) {
+        if (C_::CONCAT)
+          for (int i = et; i < BN * 32; i += 256) {
+            const int n = i >> 5, k = kb * 32 + (i & 31);
+            put(b_z(kb), n, k, bval(n, k, rank == 1));
+          }
+        for (int i = et; i < (BN / 2) * 32; i += 256) {
+          const int n = i >> 5, k = kb * 32 + (i & 31), f = (int)rank * (BN / 2) + n;
+          put(b_x(kb), n, k, bval(f, k, false));
+          if (THREE_X && !C_::CONCAT) put(b_lo(kb), n, k, bval(f, k, true));
+        }
+      }
+      fence_proxy_async_smem();
+      mbar_arrive_remote(mapa(smem_u32(b_full), 0));
+    }
     uint32_t ai = 0, chunk = 0;
     for (int t = cid; t < args.total; t += ncl, ++ai) {
       const HTile tl = hdecode(args, t, rank);
@@ -658,9 +716,10 @@ namespace {
 template <int GEOM>
 cudaError_t launch_halo_geo(const Problem& p, const float* x, int h, int w, int cx, int pt, int pl, int ncb,
                             const float* bt_hi, const float* bt_lo, int64_t kpad, int64_t npad, int block_n,
-                            float* out, cudaStream_t s, bool raw = false, const void* s2d_steps = nullptr) {
+                            float* out, cudaStream_t s, bool raw = false, const void* s2d_steps = nullptr,
+                            const float* c4_filt = nullptr, bool c4_three_x = false) {
   using G_ = Geo<GEOM>;
-  const bool three_x = bt_lo != nullptr;
+  const bool three_x = GEOM == G3C4 ? c4_three_x : bt_lo != nullptr;
   HArgs a{};
   a.trace = gemm2_trace_record();
   a.kbu = Geo<GEOM>::KB_PER_UNIT;
@@ -708,7 +767,14 @@ cudaError_t launch_halo_geo(const Problem& p, const float* x, int h, int w, int 
                                GEOM == GS2D ? (int)CU_TENSOR_MAP_SWIZZLE_64B : (int)CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
   }
-  {
+  if (GEOM == G3C4) {  // B is built in the kernel from the filter: no B maps (the slots hold the X map)
+    a.w = c4_filt;
+    a.wc = p.C;
+    a.wf = (int)p.F;
+    a.wbulk = (reinterpret_cast<uintptr_t>(c4_filt) & 15) == 0 && (9 * p.C * p.F) % 4 == 0 &&
+              getenv("CONV2D_C4_NO_WBULK") == nullptr;
+    tbh = tbhf = tblf = tx;
+  } else {
     const uint64_t dims[3] = {(uint64_t)kpad, (uint64_t)npad, 1};
     const uint64_t st[2] = {(uint64_t)kpad * 4, (uint64_t)kpad * 4 * npad};
     const uint32_t box[3] = {32, (uint32_t)block_n / 2, 1};
@@ -795,25 +861,6 @@ __global__ void s2d_filter_kernel(const float* __restrict__ w, int KH, int KW, i
     if (bt_lo) bt_lo[i] = v - h;
   }
 }
-// Bt[f][k] (npad x 64, K-major) for G3C4: k = 8 * step + j, step (r, q) = (step / 2, step % 2) < 6,
-// tap s = 2q + j / 4, channel c = j % 4  <-  w[r][s][c][f] (zero for s = 3, c >= C, f >= F, steps 6, 7)
-__global__ void c4_filter_kernel(const float* __restrict__ w, int C, int F, int64_t npad, float* __restrict__ bt_hi,
-                                 float* __restrict__ bt_lo) {
-  pdl_trigger();
-  pdl_wait();
-  const int64_t total = npad * 64;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int k = (int)(i % 64);
-    const int f = (int)(i / 64);
-    const int step = k / 8, j = k % 8;
-    const int r = step / 2, sc = 2 * (step % 2) + j / 4, c = j % 4;
-    float v = 0.f;
-    if (step < 6 && sc < 3 && c < C && f < F) v = w[((int64_t)(r * 3 + sc) * C + c) * F + f];
-    const float h = bt_lo ? tf32_hi(v) : v;
-    bt_hi[i] = h;
-    if (bt_lo) bt_lo[i] = v - h;
-  }
-}
 }  // namespace
 
 cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_hi, const float* bt_lo, int64_t kpad,
@@ -829,24 +876,13 @@ bool c4_ok(const Problem& p) {
          (int64_t)p.N * ((p.HO + TH - 1) / TH) * ((p.WO + TW - 1) / TW) < (1 << 30);
 }
 
-size_t c4_workspace(const Problem& p, int block_n, bool three_x) {
-  const int64_t npad = (p.F + block_n - 1) / block_n * block_n;
-  const size_t bt = (size_t)((npad * 64 * 4 + 255) / 256 * 256);
-  return bt * (three_x ? 2 : 1);
-}
+size_t c4_workspace(const Problem&, int, bool) { return 0; }  // B is built inside the kernel
 
-cudaError_t launch_gemm_c4(const Problem& p, const float* in, const float* filt, int block_n, bool three_x, void* ws,
+cudaError_t launch_gemm_c4(const Problem& p, const float* in, const float* filt, int block_n, bool three_x, void*,
                            float* out, cudaStream_t s) {
   const int64_t npad = (p.F + block_n - 1) / block_n * block_n;
-  const size_t bt = (size_t)((npad * 64 * 4 + 255) / 256 * 256);
-  float* bt_hi = static_cast<float*>(ws);
-  float* bt_lo = three_x ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + bt) : nullptr;
-  const int64_t fb = (npad * 64 + 255) / 256;
-  const cudaError_t e =
-      launch_k(c4_filter_kernel, dim3((unsigned)fb), dim3(256), 0, s, filt, p.C, p.F, npad, bt_hi, bt_lo);
-  if (e != cudaSuccess) return e;
-  return launch_halo_geo<G3C4>(p, in, p.H, p.W, 4, p.pad_top, p.pad_left, 1, bt_hi, bt_lo, 64, npad, block_n, out, s,
-                               true);
+  return launch_halo_geo<G3C4>(p, in, p.H, p.W, 4, p.pad_top, p.pad_left, 1, nullptr, nullptr, 64, npad, block_n, out,
+                               s, true, nullptr, filt, three_x);
 }
 
 size_t s2d_workspace(const Problem& p, int block_n, bool three_x) {

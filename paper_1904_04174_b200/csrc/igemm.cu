@@ -223,7 +223,7 @@ size_t igemm_workspace(const Problem& p, bool is_1x1) {
 int igemm_launches(const Problem& p, bool is_1x1) {
   const Plan pl = make_plan(p, is_1x1, variant_of(p, is_1x1));
   if (pl.a_mode == A_S2D) return (p.C <= 3 && ((int64_t)p.W * p.C) % 4 == 0) ? 2 : 3;  // [s2d input,] filter, GEMM
-  if (pl.a_mode == A_C4) return 2;                                                      // filter, GEMM
+  if (pl.a_mode == A_C4) return 1;  // the GEMM builds B from the filter itself
   return (pl.b_mn ? 1 : 2) + (pl.pad ? 1 : 0) + (pl.splits > 1 || pl.rsplit ? 1 : 0);
 }
 
