@@ -442,12 +442,12 @@ def step_trace(args, C, convs, ws, flush):
         start = min(c[0] for c in ctas)
         t0 = start if t0 is None else t0
         end = max(c[7] for c in ctas)
-        med = lambda k: statistics.median([c[k] for c in ctas if c[k]]) if any(c[k] for c in ctas) else None
+        med = lambda j: statistics.median([c[j] for c in ctas if c[j]]) if any(c[j] for c in ctas) else None
         ent = {"conv": i, "layer": cv["layer"].name, "algo": C.ALGO_NAMES[cv["algo"]], "ctas": len(ctas),
                "start_us": round((start - t0) / 1e3, 2), "span_us": round((end - start) / 1e3, 2),
                "gap_before_us": round((start - prev_end) / 1e3, 2) if prev_end else None}
-        for k, nm in ((1, "setup"), (3, "mma0"), (5, "last_store")):
-            m = med(k)
+        for slot, nm in ((1, "setup"), (3, "mma0"), (5, "last_store")):
+            m = med(slot)
             ent[nm + "_med_us"] = round((m - start) / 1e3, 2) if m else None
         ent["exit_med_us"] = round((med(7) - start) / 1e3, 2)
         out.append(ent)
