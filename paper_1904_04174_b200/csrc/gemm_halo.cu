@@ -14,8 +14,10 @@
 // computed once per halo instead of once per tap.
 //
 // Same warp roles as gemm2sm.cu (0-3 transform, 4 TMA producer, 5 MMA issuer + TMEM, 6-9
-// epilogue), same CTA pair (cta_group::2, M = 256 = two independent 8x16 spatial tiles), two
-// rings: halo slots (TMA -> transform -> MMA) and B stages (2-CTA TMA straight to the leader).
+// epilogue; G3C4: 6-13), same CTA pair (cta_group::2, M = 256 = two independent 8x16 spatial tiles),
+// two rings: halo slots (TMA -> transform -> MMA) and B stages (2-CTA TMA straight to the leader).
+// Three geometries share the kernel (see Geo): G3X3 (C % 32 == 0), GS2D (the space-to-depth stem)
+// and G3C4 (3x3 with C <= 4: 16-byte pixels, two taps per K=8 step, B built in the kernel).
 #include <cstdlib>
 
 #include "gemm2sm.h"
