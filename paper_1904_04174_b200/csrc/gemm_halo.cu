@@ -16,8 +16,9 @@
 // Same warp roles as gemm2sm.cu (0-3 transform, 4 TMA producer, 5 MMA issuer + TMEM, 6-9
 // epilogue; G3C4: 6-13), same CTA pair (cta_group::2, M = 256 = two independent 8x16 spatial tiles),
 // two rings: halo slots (TMA -> transform -> MMA) and B stages (2-CTA TMA straight to the leader).
-// Three geometries share the kernel (see Geo): G3X3 (C % 32 == 0), GS2D (the space-to-depth stem)
-// and G3C4 (3x3 with C <= 4: 16-byte pixels, two taps per K=8 step, B built in the kernel).
+// Four geometries share the kernel (see Geo): G3X3 (C % 32 == 0), GS2D / GS2P (the space-to-depth stem,
+// 64-byte SW64 pixels / packed 16-byte chunk planes) and G3C4 (3x3 with C <= 4: 16-byte pixels, two taps
+// per K=8 step, B built in the kernel).
 #include <cstdlib>
 
 #include "gemm2sm.h"
@@ -45,15 +46,23 @@ constexpr int HWD = 16;                   // halo box width (pixels) = 8-row gro
 //             matrix column (channels of tap s+1) starts ONE pixel later (LBO = 16 B; SBO = 16 halo pixels =
 //             one output row) -- overlapping views, no data replicated.  Six steps (r, s in {0, 2}; the s = 3
 //             half has zero B) = two k-blocks, against 16 for a 32-channel-padded tap.
-enum { G3X3 = 0, GS2D = 1, G3C4 = 2 };
+//   GS2P (3): the space-to-depth stem with the s2d pixel split into C planes of 16-byte chunks (plane q =
+//             slots 4q..4q+3 of every X' pixel; the all-zero 16-byte chunks of C = 3 are not stored).  A K=8
+//             step pairs ANY two (tap, plane) chunks that carry a real (tap, slot): its A view is a
+//             no-swizzle K-major descriptor at the first chunk with LBO = the distance to the second, so the
+//             step list packs the real chunks densely: C = 3, 7x7 -> 43 chunks = 22 steps (176 K-slots)
+//             against GS2D's 28 steps (224) -- a 0.835 instead of 0.656 ceiling on the 147 real MACs.
+enum { G3X3 = 0, GS2D = 1, G3C4 = 2, GS2P = 3 };
 template <int GEOM>
 struct Geo {
-  static constexpr int TAPW = GEOM == GS2D ? 4 : 3;     // taps per filter row
+  static constexpr bool S2D = GEOM == GS2D || GEOM == GS2P;  // stride-2 stems over s2d halos
+  static constexpr int TAPW = S2D ? 4 : 3;              // taps per filter row
   static constexpr int HHT = TH + TAPW - 1;             // halo box height
-  static constexpr int ROWB = GEOM == GS2D ? 64 : GEOM == G3C4 ? 16 : 128;  // bytes per halo pixel
+  static constexpr int ROWB = GEOM == GS2D ? 64 : (GEOM == G3C4 || GEOM == GS2P) ? 16 : 128;  // bytes per halo pixel
   static constexpr int HALO_ROWS = HWD * HHT;
-  static constexpr int HALO_BYTES = (HALO_ROWS * ROWB + 1023) / 1024 * 1024;
-  static constexpr int KB_PER_UNIT = GEOM == GS2D ? 8 : GEOM == G3C4 ? 2 : 9;  // 32-wide k-blocks per unit
+  static constexpr int PLANE_BYTES = HALO_ROWS * ROWB;  // GS2P: one 16-byte-chunk plane
+  static constexpr int HALO_BYTES = ((GEOM == GS2P ? 3 : 1) * HALO_ROWS * ROWB + 1023) / 1024 * 1024;
+  static constexpr int KB_PER_UNIT = GEOM == GS2D ? 8 : GEOM == GS2P ? 6 : GEOM == G3C4 ? 2 : 9;  // k-blocks per unit
   static constexpr bool RAWG = GEOM != G3X3;           // halo built from raw patches, K steps from a table
   // epilogue warps: G3C4 tiles are short (six K=8 steps), so the per-tile epilogue chain (TMEM load ->
   // smem stage -> proxy fence -> TMA store) is the critical path; two warps per TMEM lane quarter, each
@@ -78,6 +87,7 @@ struct HArgs {
   // C = 3 the second half of the a = 3 taps of a 7x7 stem; the list is padded with zero-B steps)
   // per k-block kb: the four steps' A-view offsets from the halo base, in 16-byte descriptor units (u16 x 4)
   uint64_t soff[8];
+  uint64_t slbo[8];  // GS2P: per step, the LBO (16-byte units) from the step's first chunk to its second
   int kbu;
   // G3C4: the transform warps build the resident B stages straight from the HWCF filter at kernel start
   // (no filter-prep launch, no workspace); wc / wf = the filter's C and F
@@ -89,6 +99,13 @@ struct HArgs {
 struct S2DSteps {
   uint8_t code[32];  // tap*2 + half per issued K=8 step
   int n;             // issued (non-padding) steps
+};
+
+// GS2P step list: step i multiplies chunks c1[i] (k = 8i..8i+3) and c2[i] (k = 8i+4..8i+7), chunk code =
+// tap*4 + plane (tap = a*4 + e); c2 = 0xFF: the second half of the step is zero B (odd chunk count)
+struct S2PSteps {
+  uint8_t c1[32], c2[32];
+  int n;
 };
 
 constexpr int RAW_ROWS = 2 * (TH + 3);  // 38 input rows behind a 19-row s2d halo
@@ -126,11 +143,14 @@ struct HCfg {
   static constexpr int ACC = CONCAT ? 2 * BN : BN;                     // TMEM columns per accumulator
   static constexpr int EPI = Geo<GEOM>::EW * 2 * 32 * 128;
   static_assert(GEOM != G3C4 || EPI >= 9 * 4 * 128 * 4, "G3C4 stages the filter in the epilogue buffers");
-  static constexpr int RAWB = Geo<GEOM>::RAWG ? RAW_BYTES_MAX : 0;      // raw-patch staging
   // raw-patch ring: G3C4 patches are small (18 rows x 48 floats at most), so four are in flight -- a single
-  // slot serialises every tile behind one TMA round trip (measured: 1.6 us per tile on VGG conv1_1)
-  static constexpr int NR = GEOM == G3C4 ? 4 : 1;
-  static constexpr int RAW_SLOT = GEOM == G3C4 ? (RAW_ROWS_C4 * raw_row_floats_c4(4) * 4 + 127) / 128 * 128 : 0;
+  // slot serialises every tile behind one TMA round trip (measured: 1.6 us per tile on VGG conv1_1); GS2P's
+  // smaller halo leaves room for two stem patches
+  static constexpr int NR = GEOM == G3C4 ? 4 : GEOM == GS2P ? 2 : 1;
+  static constexpr int RAW_SLOT = GEOM == G3C4   ? (RAW_ROWS_C4 * raw_row_floats_c4(4) * 4 + 127) / 128 * 128
+                                  : GEOM == GS2P ? (RAW_BYTES_MAX + 127) / 128 * 128
+                                                 : 0;
+  static constexpr int RAWB = !Geo<GEOM>::RAWG ? 0 : (NR * RAW_SLOT > RAW_BYTES_MAX ? NR * RAW_SLOT : RAW_BYTES_MAX);
   static_assert(NR * RAW_SLOT <= RAWB, "raw ring");
   static constexpr int BUDGET = 232448 - EPI - RAWB - 1024 - 512 - HS * HSLOT;
   // BRES (GS2D with CONCAT or TF32): the whole B (8 k-blocks, K = 256) stays resident -- stage kb holds
@@ -261,7 +281,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
           const int r = u % C_::NR;
           if (u >= C_::NR) mbar_wait(&raw_empty[r], ((u / C_::NR) - 1) & 1);
           mbar_arrive_expect_tx(&raw_ld[r], (uint32_t)(raw_rows<GEOM>() * raw_floats<GEOM>(args.rc) * 4));
-          const int sc = GEOM == GS2D ? 2 : 1;  // input pixels per output pixel
+          const int sc = G_::S2D ? 2 : 1;  // input pixels per output pixel
           const int col0 = (sc * tl.wo0 - args.rpl) * args.rc;
           tma_load_3d(&tmX, &raw_ld[r], smem_u32(raw + r * C_::RAW_SLOT), col0 - (col0 & 3), sc * tl.ho0 - args.rpt,
                       tl.n);
@@ -331,6 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
       for (int t = cid; t < args.total; t += ncl, ++ai) {
         const int acc = (int)(ai % C_::NACC);
         uint64_t soff_next = G_::RAWG ? args.soff[0] : 0;  // GS2D / G3C4: next k-block's view offsets, a step ahead
+        uint64_t slbo_next = GEOM == GS2P ? args.slbo[0] : 0;
         if (ai >= (uint32_t)C_::NACC) mbar_wait(&tmem_empty[acc], ((ai / C_::NACC) - 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * C_::ACC);
@@ -359,8 +380,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
             continue;
           }
           for (int kb = 0; kb < KBU; ++kb, ++bit) {
-            const uint64_t soff = soff_next;
+            const uint64_t soff = soff_next, slbo = slbo_next;
             if constexpr (G_::RAWG) soff_next = args.soff[kb + 1 < 8 ? kb + 1 : 7];
+            if constexpr (GEOM == GS2P) slbo_next = args.slbo[kb + 1 < 8 ? kb + 1 : 7];
             const int s = C_::BRES ? kb : (int)(bit % S);
             if (!C_::BRES) {
               mbar_wait(&b_full[s], (bit / S) & 1);
@@ -375,6 +397,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
               const uint32_t a = base + (uint32_t)((r * HWD + c) * G_::ROWB);
               return GEOM == GS2D   ? umma_desc_sw64_kmajor_sbo(a, HWD * G_::ROWB)
                      : GEOM == G3C4 ? umma_desc_interleave_kmajor(a, 16u, HWD * G_::ROWB)  // LBO: next pixel
+                     : GEOM == GS2P ? umma_desc_interleave_kmajor(a, 0u, HWD * G_::ROWB)   // LBO per step
                                     : umma_desc_sw128_kmajor_sbo(a, HWD * G_::ROWB, 0u);
             };
             if constexpr (C_::ATM) {  // A from the TMEM tap slot the transform warps filled
@@ -414,7 +437,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
               // table: the tap's view plus 32 bytes for the second 8 slots (uniform arithmetic, no branch)
               uint64_t dah, dal;
               if constexpr (G_::RAWG) {
-                const uint64_t off = (soff >> (16 * k)) & 0xFFFFu;
+                uint64_t off = (soff >> (16 * k)) & 0xFFFFu;
+                if constexpr (GEOM == GS2P) off += ((slbo >> (16 * k)) & 0xFFFFu) << 16;  // LBO field
                 dah = dah0 + off;
                 dal = dal0 + off;
               } else {
@@ -515,16 +539,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
           mbar_arrive_remote(h_full_leader + (uint32_t)(h * sizeof(uint64_t)));
           continue;
         }
-        if (GEOM == GS2D && args.raw) {
+        if (G_::S2D && args.raw) {
           // build the s2d halo: pixel p = (hi, wi) of the 19 x 16 halo, 16-byte chunk k = slots 4k..4k+3,
-          // slot = (b*2 + d)*C + c <- raw[2*hi + b][2*wi + d][c]; SWIZZLE_64B placement (chunk k of the
-          // 64-byte pixel row goes to k ^ ((p >> 1) & 3)), as the TMA would have written X'
-          mbar_wait(raw_ld, hit & 1);
+          // slot = (b*2 + d)*C + c <- raw[2*hi + b][2*wi + d][c]; GS2D: SWIZZLE_64B placement (chunk k of the
+          // 64-byte pixel row goes to k ^ ((p >> 1) & 3)), as the TMA would have written X'; GS2P: chunk k
+          // is pixel p of plane k (planes k < C only)
+          const int rs = (int)(hit % C_::NR);
+          mbar_wait(&raw_ld[rs], (hit / C_::NR) & 1);
           if (hit >= (uint32_t)HS) mbar_wait(&h_empty[h], ((hit / HS) - 1) & 1);  // the MMAs released the slot
           const HTile tl = hdecode(args, tt, rank);
           const int C = args.rc, rowf = raw_row_floats(C);
           const int shift = ((2 * tl.wo0 - args.rpl) * C) & 3;  // patch origin within the aligned load
-          const uint32_t rb = smem_u32(raw), hh = smem_u32(halo_hi(h)), hl = smem_u32(halo_lo(h));
+          const uint32_t rb = smem_u32(raw + rs * C_::RAW_SLOT), hh = smem_u32(halo_hi(h)), hl = smem_u32(halo_lo(h));
           // thread t always handles chunk k = t & 3 of pixels p = (t >> 2) + 32 j: column wc and the swizzle
           // phase are fixed, the halo row advances by 2 per step -- all index math hoisted
           const int k = t & 3, p0 = t >> 2;
@@ -537,19 +563,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
             soff[e] = bd < 4 ? (bd >> 1) * rowf + shift + (2 * wc + (bd & 1)) * C + c : -1;
           }
           const uint32_t chunk_off = (uint32_t)((k ^ ((p0 >> 1) & 3)) << 4);
-          for (int p = p0; p < G_::HALO_ROWS; p += 32) {
+          const bool skip = GEOM == GS2P && k >= C;  // C planes only
+          for (int p = p0; p < G_::HALO_ROWS && !skip; p += 32) {
             const int hr = p / HWD;
             const uint32_t rrow = rb + 4u * (uint32_t)(2 * hr * rowf);
             float v[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) v[e] = soff[e] >= 0 ? lds32(rrow + 4u * (uint32_t)soff[e]) : 0.f;
-            const uint32_t off = (uint32_t)(p * 64) + chunk_off;
+            const uint32_t off = GEOM == GS2P ? (uint32_t)(k * G_::PLANE_BYTES + p * 16) : (uint32_t)(p * 64) + chunk_off;
             sts128(hh + off, make_float4(v[0], v[1], v[2], v[3]));
             if (THREE_X)
               sts128(hl + off, make_float4(v[0] - tf32_hi(v[0]), v[1] - tf32_hi(v[1]), v[2] - tf32_hi(v[2]),
                                            v[3] - tf32_hi(v[3])));
           }
-          mbar_arrive(raw_empty);
+          mbar_arrive(&raw_empty[rs]);
           fence_proxy_async_smem();
           mbar_arrive_remote(h_full_leader + (uint32_t)(h * sizeof(uint64_t)));
           continue;
@@ -735,6 +762,20 @@ cudaError_t launch_halo_geo(const Problem& p, const float* x, int h, int w, int 
     }
     a.kbu = (st->n + 3) / 4;
   }
+  if (GEOM == GS2P && s2d_steps) {  // chunk pairs: view at the first chunk, LBO to the second
+    const auto* st = static_cast<const S2PSteps*>(s2d_steps);
+    auto addr16 = [](int code) {  // chunk address in 16-byte units from the halo base
+      const int tap = code >> 2, plane = code & 3;
+      return (plane * Geo<GS2P>::PLANE_BYTES + ((tap >> 2) * HWD + (tap & 3)) * 16) >> 4;
+    };
+    for (int i = 0; i < 32; ++i) {
+      const int o1 = addr16(st->c1[i]);
+      const int lbo = st->c2[i] == 0xFF ? 0 : addr16(st->c2[i]) - o1;
+      a.soff[i / 4] |= (uint64_t)o1 << (16 * (i % 4));
+      a.slbo[i / 4] |= (uint64_t)lbo << (16 * (i % 4));
+    }
+    a.kbu = (st->n + 3) / 4;
+  }
   a.N = p.N; a.H = h; a.W = w; a.HO = p.HO; a.WO = p.WO; a.PT = pt; a.PL = pl;
   a.ncb = ncb;
   a.tiles_w = (p.WO + TW - 1) / TW;
@@ -863,6 +904,32 @@ __global__ void s2d_filter_kernel(const float* __restrict__ w, int KH, int KW, i
     if (bt_lo) bt_lo[i] = v - h;
   }
 }
+// Bt'[f][k] (npad x 192, K-major) for GS2P: k = 8 * step + j, chunk = j < 4 ? c1 : c2 (tap (a, e), plane q),
+// slot = 4q + j % 4 = (b*2 + d)*C + c  <-  w[2a+b][2e+d][c][f] (zero past K, past 4C slots, for c2 = 0xFF and
+// for steps past st.n); 3xTF32: hi/lo
+__global__ void s2p_filter_kernel(const float* __restrict__ w, int KH, int KW, int C, int F, int64_t npad,
+                                  float* __restrict__ bt_hi, float* __restrict__ bt_lo, const S2PSteps st) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int KP = Geo<GS2P>::KB_PER_UNIT * 32;
+  const int64_t total = npad * KP;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % KP);
+    const int f = (int)(i / KP);
+    const int step = k / 8, j = k % 8;
+    const int code = step < st.n ? (j < 4 ? st.c1[step] : st.c2[step]) : 0xFF;
+    float v = 0.f;
+    if (code != 0xFF && f < F) {
+      const int tap = code >> 2, plane = code & 3, a = tap >> 2, e = tap & 3;
+      const int slot = 4 * plane + (j & 3), bd = slot / C, c = slot % C;
+      const int r = 2 * a + (bd >> 1), sc = 2 * e + (bd & 1);
+      if (bd < 4 && r < KH && sc < KW) v = w[((int64_t)(r * KW + sc) * C + c) * F + f];
+    }
+    const float h = bt_lo ? tf32_hi(v) : v;
+    bt_hi[i] = h;
+    if (bt_lo) bt_lo[i] = v - h;
+  }
+}
 }  // namespace
 
 cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_hi, const float* bt_lo, int64_t kpad,
@@ -922,6 +989,38 @@ cudaError_t launch_gemm_s2d(const Problem& p, const float* in, const float* filt
   for (int c = st.n; c < 32; ++c) st.code[c] = st.code[0];  // padding steps: any view, zero B rows
   // raw mode (C <= 3, 16-byte input rows): the GEMM builds s2d halos from raw input patches itself
   const bool raw = p.C <= 3 && ((int64_t)p.W * p.C) % 4 == 0 && getenv("CONV2D_S2D_PREPASS") == nullptr;
+  if (raw && getenv("CONV2D_S2D_SW64") == nullptr) {
+    // GS2P: the (tap, plane) chunks with a real (tap, slot), in halo-address order, paired into K=8 steps
+    S2PSteps sp{};
+    int chunks[64], nc = 0;
+    for (int plane = 0; plane < p.C; ++plane)
+      for (int tap = 0; tap < 16; ++tap) {
+        const int a_ = tap >> 2, e_ = tap & 3;
+        bool any = false;
+        for (int j = 0; j < 4 && !any; ++j) {
+          const int slot = 4 * plane + j, bd = slot / p.C;
+          any = bd < 4 && 2 * a_ + (bd >> 1) < p.KH && 2 * e_ + (bd & 1) < p.KW;
+        }
+        if (any) chunks[nc++] = tap * 4 + plane;
+      }
+    // address order = (plane, a, e): already ascending by construction (plane-major, tap = a*4 + e)
+    for (int i = 0; i < nc; i += 2) {
+      sp.c1[sp.n] = (uint8_t)chunks[i];
+      sp.c2[sp.n] = i + 1 < nc ? (uint8_t)chunks[i + 1] : (uint8_t)0xFF;
+      ++sp.n;
+    }
+    for (int i = sp.n; i < 32; ++i) {  // padding steps: any view, zero B rows
+      sp.c1[i] = sp.c1[0];
+      sp.c2[i] = 0xFF;
+    }
+    if (sp.n > 4 * Geo<GS2P>::KB_PER_UNIT) return cudaErrorInvalidValue;
+    constexpr int KP = Geo<GS2P>::KB_PER_UNIT * 32;
+    const int64_t fb = (npad * KP + 255) / 256;
+    cudaError_t e = launch_k(s2p_filter_kernel, dim3((unsigned)fb), dim3(256), 0, s, filt, p.KH, p.KW, p.C, p.F,
+                             npad, bt_hi, bt_lo, sp);
+    if (e != cudaSuccess) return e;
+    return launch_halo_geo<GS2P>(p, in, hs, wsd, 16, 0, 0, 1, bt_hi, bt_lo, KP, npad, block_n, out, s, true, &sp);
+  }
   if (raw) {
     int64_t fb = (npad * 256 + 255) / 256;
     cudaError_t e = launch_k(s2d_filter_kernel, dim3((unsigned)fb), dim3(256), 0, s, filt, p.KH, p.KW, p.C, p.F,

@@ -25,8 +25,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=2000)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--focus", choices=["all", "c4"], default="all",
-                    help="c4: only 3x3 / stride 1 with C <= 4 (implicit_gemm's A_C4 4-channel halo path)")
+    ap.add_argument("--focus", choices=["all", "c4", "s2d"], default="all",
+                    help="c4: only 3x3 / stride 1 with C <= 4 (implicit_gemm's A_C4 4-channel halo path); "
+                         "s2d: only 7x7 / 8x8 stride-2 stems with C <= 4 (the space-to-depth halo paths)")
     args = ap.parse_args()
 
     import torch
@@ -52,6 +53,14 @@ def main():
             c = int(rng.choice([1, 2, 3, 4]))
             w = int(rng.integers(1, 40)) * (4 // np.gcd(c, 4))  # W*C % 4 == 0 (raw 16-byte rows)
             h = int(rng.integers(1, 72))
+            f = int(rng.choice([1, 3, 8, 17, 32, 36, 64, 96, 100, 128]))
+        if args.focus == "s2d":
+            k = int(rng.choice([7, 8]))
+            kw = int(rng.choice([7, 8]))
+            s = 2
+            c = int(rng.choice([1, 2, 3, 3, 4]))
+            w = int(rng.integers(kw, 90))
+            h = int(rng.integers(k, 90))
             f = int(rng.choice([1, 3, 8, 17, 32, 36, 64, 96, 100, 128]))
         pad = int(rng.integers(0, 2))
         math = int(rng.integers(0, 2))
