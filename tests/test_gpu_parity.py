@@ -425,6 +425,37 @@ def test_igemm_c4_halo(cuda_ok, monkeypatch, case):
             assert_int_exact(p, gpu_conv(p, xi, wi, a), refi, deni, a, f"c4 int v{variant} {case} math={math}")
 
 
+S2D_CASES = [  # 7x7 / 8x8 stride-2 stems with C <= 3 and W*C % 4 == 0: raw-patch s2d halos
+    (1, 37, 28, 3, 64, 7, 7, 2, 2, 0),     # ragged 8x16 tiles, SAME corners
+    (2, 40, 36, 1, 32, 7, 7, 2, 2, 1),     # C = 1, VALID
+    (1, 33, 48, 2, 100, 8, 8, 2, 2, 0),    # C = 2, K = 8, F not a multiple of 32 (BN = 128)
+    (2, 24, 20, 3, 17, 7, 8, 2, 2, 0),     # non-square window, F % 4 != 0
+]
+
+
+@pytest.mark.parametrize("case", S2D_CASES, ids=str)
+def test_s2d_stem_packed_and_sw64(cuda_ok, monkeypatch, case):
+    """implicit_gemm's space-to-depth stem in both halo forms: the packed chunk-plane halo (GS2P, default:
+    K=8 steps pair arbitrary real (tap, plane) chunks through the descriptor LBO) and the SWIZZLE_64B halo
+    (GS2D, CONV2D_S2D_SW64): each against the oracle, integer-exact and within tolerance, both math modes."""
+    p0 = P(*case)
+    x, w = make_inputs(p0, layer_id=970)
+    ref, den = O.conv2d(oparams(p0), x, w, with_denom=True)
+    xi, wi = make_inputs(p0, layer_id=971, dist=synth.DIST_INT5)
+    refi, deni = O.conv2d(oparams(p0), xi, wi, with_denom=True)
+    a = C().ALGO_IMPLICIT_GEMM
+    monkeypatch.setenv("CONV2D_FORCE_VARIANT", "0")
+    for sw64 in (False, True):
+        if sw64:
+            monkeypatch.setenv("CONV2D_S2D_SW64", "1")
+        else:
+            monkeypatch.delenv("CONV2D_S2D_SW64", raising=False)
+        for math in MATHS:
+            p = p0.replace(math=math)
+            check_close(p, gpu_conv(p, x, w, a), ref, den, a, f"s2d sw64={sw64} {case} math={math}")
+            assert_int_exact(p, gpu_conv(p, xi, wi, a), refi, deni, a, f"s2d int sw64={sw64} {case} math={math}")
+
+
 WINO_FUSED_CASES = [l.params(1) for l in ALL_SHAPES if l.window == 3 and l.stride == 1 and l.channels >= 32] + [
     dict(batch=3, in_rows=15, in_cols=9, channels=64, features=68, window_rows=3, window_cols=3, stride_rows=1,
          stride_cols=1, padding=1),    # VALID, ragged tile blocks, F % 32 != 0
