@@ -61,8 +61,11 @@ cudaError_t launch_gemm_c4(const Problem& p, const float* in, const float* filt,
 size_t s2d_workspace(const Problem& p, int block_n, bool three_x);
 cudaError_t launch_gemm_s2d(const Problem& p, const float* in, const float* filt, int block_n, bool three_x,
                             void* ws, float* out, cudaStream_t s);
+// bmn: B straight from the HWCF filter `filt` (MN-major, F % 32 == 0; bt_hi / bt_lo unused), else from the
+// K-major Bt hi [/ lo] filter_prep2 wrote
 cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_hi, const float* bt_lo, int64_t kpad,
-                             int64_t npad, int block_n, float* out, cudaStream_t s);
+                             int64_t npad, int block_n, float* out, cudaStream_t s, const float* filt, bool bmn,
+                             bool three_x);
 bool gemm2_encode_tiled_sw(CUtensorMap* m, int rank, const void* base, const uint64_t* dims, const uint64_t* strides,
                            const uint32_t* box, int swizzle);  // swizzle: a CUtensorMapSwizzle value
 // same with TMA traversal strides (elem_strides[i] in [1, 8]; dimension i then loads ceil(box[i] / stride) elements)

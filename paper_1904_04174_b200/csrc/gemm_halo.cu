@@ -122,7 +122,7 @@ template <int GEOM> __host__ __device__ constexpr int raw_floats(int c) {
   return GEOM == G3C4 ? raw_row_floats_c4(c) : raw_row_floats(c);
 }
 
-template <int BN, bool THREE_X, int GEOM>
+template <int BN, bool THREE_X, int GEOM, bool BMN = false>
 struct HCfg {
   static constexpr int HALO_BYTES = Geo<GEOM>::HALO_BYTES;
   static constexpr int BHALF = (BN / 2) * BK * 4;
@@ -138,7 +138,11 @@ struct HCfg {
   // B_hi, CTA1: B_lo) for one N'=2BN MMA hi x [B_hi | B_lo] -- A_hi is read once for both products --
   // plus X = BN/2 rows of B_hi (this CTA's half) for lo x B_hi; the epilogue adds the two column halves.
   // Otherwise (BN = 128, TF32): X = B_hi half [+ B_lo half], three / one MMAs per K step.
-  static constexpr bool CONCAT = THREE_X && BN == 64;
+  // BMN (G3X3, F % 32 == 0): B streams straight from the HWCF filter as an MN-major operand (no filter-prep
+  // launch); 3xTF32 then splits B_lo in smem (warps 6+EW .. 9+EW) and uses the plain three-MMA form
+  static constexpr bool CONCAT = THREE_X && BN == 64 && !BMN;
+  static constexpr bool BSPLIT = BMN && THREE_X;
+  static constexpr int NT = Geo<GEOM>::NT + (BSPLIT ? 128 : 0);
   static constexpr int BSTAGE = CONCAT ? BFULL + BHALF : (THREE_X ? 2 : 1) * BHALF;
   static constexpr int ACC = CONCAT ? 2 * BN : BN;                     // TMEM columns per accumulator
   static constexpr int EPI = Geo<GEOM>::EW * 2 * 32 * 128;
@@ -152,13 +156,13 @@ struct HCfg {
                                                  : 0;
   static constexpr int RAWB = !Geo<GEOM>::RAWG ? 0 : (NR * RAW_SLOT > RAW_BYTES_MAX ? NR * RAW_SLOT : RAW_BYTES_MAX);
   static_assert(NR * RAW_SLOT <= RAWB, "raw ring");
-  static constexpr int BUDGET = 232448 - EPI - RAWB - 1024 - 512 - HS * HSLOT;
+  static constexpr int BUDGET = 232448 - EPI - RAWB - 1024 - 1024 - HS * HSLOT;
   // BRES (GS2D with CONCAT or TF32): the whole B (8 k-blocks, K = 256) stays resident -- stage kb holds
   // k-block kb for the kernel's lifetime; otherwise B streams through an S-stage ring per unit.
   static constexpr bool BRES = Geo<GEOM>::RAWG && (CONCAT || !THREE_X || GEOM == G3C4);
   static constexpr int S = BRES ? Geo<GEOM>::KB_PER_UNIT : ((BUDGET / BSTAGE) > 12 ? 12 : (BUDGET / BSTAGE));
   static_assert(!BRES || S * BSTAGE <= BUDGET, "resident B does not fit");
-  static constexpr int SMEM = HS * HSLOT + S * BSTAGE + EPI + RAWB + 1024 + 512;
+  static constexpr int SMEM = HS * HSLOT + S * BSTAGE + EPI + RAWB + 1024 + 1024;
   static constexpr int AS = ATM ? (512 - 2 * ACC) / 64 : 0;            // ATM: TMEM tap slots
   static constexpr uint32_t A_COL0 = 2 * ACC;                            // first column of the tap slots
   // accumulator buffers: G3C4 (short tiles) keeps four in TMEM so the epilogue of tile i overlaps the
@@ -166,7 +170,7 @@ struct HCfg {
   static constexpr int NACC = GEOM == G3C4 ? 4 : 2;
   static constexpr uint32_t TMEM_COLS = ATM ? 512 : NACC * ACC;
   static_assert(S >= 2, "halo kernel needs >= 2 B stages");
-  static_assert(!ATM || AS >= 2, "ATM needs >= 2 TMEM tap slots");
+  static_assert(!ATM || (AS >= 2 && AS <= 8), "ATM needs 2..8 TMEM tap slots");
   static_assert(NACC * ACC <= 512, "TMEM");
 };
 
@@ -184,13 +188,13 @@ __device__ __forceinline__ HTile hdecode(const HArgs& a, int t, uint32_t rank) {
   return r;
 }
 
-template <int BN, bool THREE_X, int GEOM>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
+template <int BN, bool THREE_X, int GEOM, bool BMN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HCfg<BN, THREE_X, GEOM, BMN>::NT, 1)
     halo_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmBh,
                 const __grid_constant__ CUtensorMap tmBhF, const __grid_constant__ CUtensorMap tmBlF,
                 const __grid_constant__ CUtensorMap tmD,
                 const __grid_constant__ HArgs args) {
-  using C_ = HCfg<BN, THREE_X, GEOM>;
+  using C_ = HCfg<BN, THREE_X, GEOM, BMN>;
   using G_ = Geo<GEOM>;
   constexpr int HALO_BYTES = G_::HALO_BYTES;
   constexpr int HS = C_::HS, S = C_::S;
@@ -213,9 +217,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
   uint64_t* raw_ld = tmem_empty + C_::NACC;     // raw patch landed (TMA -> transform), per ring slot
   uint64_t* raw_empty = raw_ld + 4;      // raw patch consumed (transform -> producer), per ring slot
   uint64_t* a_full = raw_empty + 4;      // ATM: tap slot written (both CTAs' transform warps -> leader MMA)
-  uint64_t* a_empty = a_full + 4;        // ATM: tap slot read by the MMAs (commit -> transform warps)
-  uint64_t* w_ld = a_empty + 4;         // G3C4: the filter's bulk copy into the epilogue buffers landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_ld + 1);
+  uint64_t* a_empty = a_full + 8;        // ATM: tap slot read by the MMAs (commit -> transform warps)
+  uint64_t* w_ld = a_empty + 8;         // G3C4: the filter's bulk copy into the epilogue buffers landed
+  uint64_t* b_ld = w_ld + 1;            // BSPLIT: this CTA's B_hi half landed (TMA -> B-split warps), per stage
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_ld + S);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -230,13 +235,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
       mbar_init(&h_full[h], 2 * 128);
       mbar_init(&h_empty[h], C_::ATM ? 128 : 1);  // ATM: this CTA's transform threads release the halo
     }
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 8; ++i) {
       mbar_init(&a_full[i], 2 * 128);
       mbar_init(&a_empty[i], 1);
     }
     for (int s = 0; s < S; ++s) {
-      mbar_init(&b_full[s], GEOM == G3C4 ? 2 * 32 * G_::EW : 1);  // G3C4: both CTAs' epilogue threads build B
+      // G3C4: both CTAs' epilogue threads build B; BSPLIT: both CTAs' B-split threads relay their stage
+      mbar_init(&b_full[s], GEOM == G3C4 ? 2 * 32 * G_::EW : C_::BSPLIT ? 2 * 128 : 1);
       mbar_init(&b_empty[s], 1);
+      mbar_init(&b_ld[s], 1);
     }
     for (int a = 0; a < C_::NACC; ++a) {
       mbar_init(&tmem_full[a], 1);
@@ -318,6 +325,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
         for (int kb = 0; kb < KBU; ++kb, ++bit) {
           const int s = bit % S;
           if (bit >= (uint32_t)S) mbar_wait(&b_empty[s], ((bit / S) - 1) & 1);
+          if constexpr (BMN) {
+            // MN-major B_hi half straight from the HWCF filter: rows k = tap*C + cb*32 .. +31, this CTA's
+            // 32-column chunks of the pair's N tile ({n % 32, k, n / 32} view, box {32, 32, BN/64})
+            const int krow = (kb * args.ncb + cb) * BK;
+            if constexpr (C_::BSPLIT) {  // to this CTA's barrier: the B-split warps derive lo, then relay
+              mbar_arrive_expect_tx(&b_ld[s], (uint32_t)C_::BHALF);
+              tma_load_3d(&tmBh, &b_ld[s], smem_u32(b_x(s)), 0, krow, nrow / 32);
+            } else {
+              if (rank == 0) mbar_arrive_expect_tx(&b_full[s], 2 * C_::BHALF);
+              tma_load_3d_2sm(&tmBh, b_full_leader + (uint32_t)(s * sizeof(uint64_t)), smem_u32(b_x(s)), 0, krow,
+                              nrow / 32);
+            }
+            continue;
+          }
           if (rank == 0) mbar_arrive_expect_tx(&b_full[s], 2 * C_::BSTAGE);
           const uint32_t fb = b_full_leader + (uint32_t)(s * sizeof(uint64_t));
           // filter prep order k = tap * C + c: G3X3 k-block kb = tap kb, channel block cb; GS2D k-block
@@ -341,7 +362,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
   } else if (warp == 5) {
     // ============================ MMA issuer (leader) ============================
     if (rank == 0) {  // whole warp, converged: operands stay warp-uniform
-      constexpr uint32_t idesc = idesc_tf32(256, BN);
+      constexpr uint32_t idesc = idesc_tf32(256, BN) | (BMN ? IDESC_B_MN : 0u);
       constexpr uint32_t idesc2 = idesc_tf32(256, 2 * BN);  // 3x: hi x [B_hi | B_lo]
       uint32_t hit = 0, bit = 0, ai = 0, ait = 0;
       if (C_::BRES && cid < args.total) {
@@ -405,15 +426,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
               mbar_wait(&a_full[slot], (ait / C_::AS) & 1);
               tc_fence_after();
               const uint32_t ahi = tmem_base + C_::A_COL0 + (uint32_t)(slot * 64), alo = ahi + 32;
-              const uint64_t dbx = umma_desc_sw128_kmajor(smem_u32(b_x(s)));
+              // BMN: MN-major SW128_BASE32B B (32 k-rows x 128 B per 32-wide n chunk: LBO 4 KB, SBO 512 B,
+              // K=8 step = 1 KB = 64 descriptor units)
+              auto bd = [&](const uint8_t* ptr) {
+                return BMN ? umma_desc_sw128b32_mn(smem_u32(ptr), BK * 128, 512) : umma_desc_sw128_kmajor(smem_u32(ptr));
+              };
+              const uint64_t dbx = bd(b_x(s));
               const uint64_t dbz = C_::CONCAT ? umma_desc_sw128_kmajor(smem_u32(b_z(s))) : 0;
-              const uint64_t dbl = C_::CONCAT ? 0 : umma_desc_sw128_kmajor(smem_u32(b_lo(s)));
+              const uint64_t dbl = C_::CONCAT ? 0 : bd(b_lo(s));
               // the tap's four K=8 steps from one asm block (sm100.cuh mma2_kblock_tt_*)
               const uint32_t acc0 = (cb > 0 || kb > 0) ? 1u : 0u;
               if (C_::CONCAT)
                 mma2_kblock_tt_concat(d, ahi, alo, dbz, dbx, idesc2, idesc, acc0);
               else
-                mma2_kblock_tt_3x(d, ahi, alo, dbx, dbl, idesc, acc0);
+                mma2_kblock_tt_3x(d, ahi, alo, dbx, dbl, idesc, acc0, BMN ? 64u : 2u);
               if (!C_::BRES) mma_commit_2sm_mc_warp(&b_empty[s], 0x3);
               mma_commit_2sm_mc_warp(&a_empty[slot], 0x3);
               ++ait;
@@ -426,7 +452,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
             const uint64_t dbz = C_::CONCAT ? umma_desc_sw128_kmajor(smem_u32(b_z(s))) : 0;
             const uint64_t dbl = (THREE_X && !C_::CONCAT) ? umma_desc_sw128_kmajor(smem_u32(b_lo(s))) : 0;
             if constexpr (GEOM == G3X3 && !THREE_X) {  // TF32 3x3: one asm block per k-block (sm100.cuh)
-              mma2_kblock_1x_ss(d, dah0, dbx, 2, 2, idesc, (cb > 0 || kb > 0) ? 1u : 0u);
+              const uint64_t dbm = BMN ? umma_desc_sw128b32_mn(smem_u32(b_x(s)), BK * 128, 512) : dbx;
+              mma2_kblock_1x_ss(d, dah0, dbm, 2, BMN ? 64 : 2, idesc, (cb > 0 || kb > 0) ? 1u : 0u);
               if (!C_::BRES) mma_commit_2sm_mc_warp(&b_empty[s], 0x3);
               continue;
             }
@@ -595,6 +622,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
         mbar_arrive_remote(h_full_leader + (uint32_t)(h * sizeof(uint64_t)));
       }
     }
+  } else if (C_::BSPLIT && warp >= 6 + G_::EW) {
+    // ============================ B-lo split (BSPLIT: warps 6+EW .. 9+EW) ============================
+    // lo = b - trunc_tf32(b) elementwise over this CTA's B_hi half (the swizzled MN-major layout carries
+    // over), then relay the stage to the leader's b_full -- same k-block order as the producer
+    const int t2 = (int)threadIdx.x - (6 + G_::EW) * 32;
+    const uint32_t b_full_leader = mapa(smem_u32(b_full), 0);
+    uint32_t bit = 0;
+    const int my_tiles = args.total > cid ? (args.total - cid + ncl - 1) / ncl : 0;
+    for (int u = 0; u < my_tiles * args.ncb; ++u)
+      for (int kb = 0; kb < KBU; ++kb, ++bit) {
+        const int s = (int)(bit % S);
+        mbar_wait(&b_ld[s], (bit / S) & 1);
+        const uint32_t hb = smem_u32(b_x(s)), lb = smem_u32(b_lo(s));
+#pragma unroll
+        for (int i = t2 * 16; i < C_::BHALF; i += 128 * 16) {
+          const float4 v = lds128(hb + (uint32_t)i);
+          sts128(lb + (uint32_t)i, make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z),
+                                               v.w - tf32_hi(v.w)));
+        }
+        fence_proxy_async_smem();
+        mbar_arrive_remote(b_full_leader + (uint32_t)(s * sizeof(uint64_t)));
+      }
   } else {
     // ============================ epilogue (warps 6 .. 6 + EW) ============================
     // warp q = warp % 4 owns TMEM lanes [32q, 32q+32) = output rows ho0 + 4q .. +3, wo0 .. wo0+7; with
@@ -711,14 +760,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Geo<GEOM>::NT, 1)
   if (threadIdx.x == 0 && args.trace) args.trace[blockIdx.x * 8 + 7] = globaltimer_ns();
 }
 
-template <int BN, bool THREE_X, int GEOM>
+template <int BN, bool THREE_X, int GEOM, bool BMN = false>
 cudaError_t launch_h(const CUtensorMap& x, const CUtensorMap& bh, const CUtensorMap& bhf, const CUtensorMap& blf,
                      const CUtensorMap& dm, const HArgs& a, int clusters, cudaStream_t s) {
-  using C_ = HCfg<BN, THREE_X, GEOM>;
-  auto kern = halo_kernel<BN, THREE_X, GEOM>;
-  const cudaError_t e = smem_attr_once<halo_kernel<BN, THREE_X, GEOM>>(C_::SMEM);
+  using C_ = HCfg<BN, THREE_X, GEOM, BMN>;
+  auto kern = halo_kernel<BN, THREE_X, GEOM, BMN>;
+  const cudaError_t e = smem_attr_once<halo_kernel<BN, THREE_X, GEOM, BMN>>(C_::SMEM);
   if (e != cudaSuccess) return e;
-  return launch_k(kern, dim3(2 * clusters), dim3(Geo<GEOM>::NT), C_::SMEM, s, x, bh, bhf, blf, dm, a);
+  return launch_k(kern, dim3(2 * clusters), dim3(C_::NT), C_::SMEM, s, x, bh, bhf, blf, dm, a);
 }
 
 }  // namespace
@@ -746,9 +795,10 @@ template <int GEOM>
 cudaError_t launch_halo_geo(const Problem& p, const float* x, int h, int w, int cx, int pt, int pl, int ncb,
                             const float* bt_hi, const float* bt_lo, int64_t kpad, int64_t npad, int block_n,
                             float* out, cudaStream_t s, bool raw = false, const void* s2d_steps = nullptr,
-                            const float* c4_filt = nullptr, bool c4_three_x = false) {
+                            const float* c4_filt = nullptr, bool c4_three_x = false, bool bmn = false) {
   using G_ = Geo<GEOM>;
-  const bool three_x = GEOM == G3C4 ? c4_three_x : bt_lo != nullptr;
+  // G3C4 and BMN read the filter itself (c4_filt): the math mode comes from the caller
+  const bool three_x = (GEOM == G3C4 || bmn) ? c4_three_x : bt_lo != nullptr;
   HArgs a{};
   a.trace = gemm2_trace_record();
   a.kbu = Geo<GEOM>::KB_PER_UNIT;
@@ -817,6 +867,14 @@ cudaError_t launch_halo_geo(const Problem& p, const float* x, int h, int w, int 
     a.wbulk = (reinterpret_cast<uintptr_t>(c4_filt) & 15) == 0 && (9 * p.C * p.F) % 4 == 0 &&
               getenv("CONV2D_C4_NO_WBULK") == nullptr;
     tbh = tbhf = tblf = tx;
+  } else if (bmn) {  // MN-major B from the row-major (9C x F) filter: view {n % 32, k, n / 32}, box {32, 32, BN/64}
+    if (p.F % 32 != 0 || !c4_filt) return cudaErrorInvalidValue;
+    const uint64_t dims[3] = {32, (uint64_t)p.KH * p.KW * p.C, (uint64_t)(p.F / 32)};
+    const uint64_t st[2] = {(uint64_t)p.F * 4, 128};
+    const uint32_t box[3] = {32, 32, (uint32_t)(block_n / 64)};
+    if (!gemm2_encode_tiled_sw(&tbh, 3, c4_filt, dims, st, box, (int)CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+      return cudaErrorInvalidValue;
+    tbhf = tblf = tbh;
   } else {
     const uint64_t dims[3] = {(uint64_t)kpad, (uint64_t)npad, 1};
     const uint64_t st[2] = {(uint64_t)kpad * 4, (uint64_t)kpad * 4 * npad};
@@ -842,6 +900,17 @@ cudaError_t launch_halo_geo(const Problem& p, const float* x, int h, int w, int 
   }
   if (!a.tma_store) td = tbh;
   const int clusters = a.total < 74 ? a.total : 74;
+  if constexpr (GEOM == G3X3) {
+    if (bmn) {
+      switch (block_n) {
+        case 64: return three_x ? launch_h<64, true, GEOM, true>(tx, tbh, tbhf, tblf, td, a, clusters, s)
+                                : launch_h<64, false, GEOM, true>(tx, tbh, tbhf, tblf, td, a, clusters, s);
+        case 128: return three_x ? launch_h<128, true, GEOM, true>(tx, tbh, tbhf, tblf, td, a, clusters, s)
+                                 : launch_h<128, false, GEOM, true>(tx, tbh, tbhf, tblf, td, a, clusters, s);
+      }
+      return cudaErrorInvalidValue;
+    }
+  }
   switch (block_n) {
     case 64: return three_x ? launch_h<64, true, GEOM>(tx, tbh, tbhf, tblf, td, a, clusters, s)
                             : launch_h<64, false, GEOM>(tx, tbh, tbhf, tblf, td, a, clusters, s);
@@ -933,9 +1002,10 @@ __global__ void s2p_filter_kernel(const float* __restrict__ w, int KH, int KW, i
 }  // namespace
 
 cudaError_t launch_gemm_halo(const Problem& p, const float* in, const float* bt_hi, const float* bt_lo, int64_t kpad,
-                             int64_t npad, int block_n, float* out, cudaStream_t s) {
+                             int64_t npad, int block_n, float* out, cudaStream_t s, const float* filt, bool bmn,
+                             bool three_x) {
   return launch_halo_geo<G3X3>(p, in, p.H, p.W, p.C, p.pad_top, p.pad_left, p.C / 32, bt_hi, bt_lo, kpad, npad,
-                               block_n, out, s);
+                               block_n, out, s, false, nullptr, filt, three_x, bmn);
 }
 
 // G3C4: 3x3 / stride 1 with C <= 4, raw patches straight from x (16-byte rows of W*C floats)

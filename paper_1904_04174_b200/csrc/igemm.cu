@@ -138,7 +138,7 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
                   ? gemm2_choose_splits(p.M(), p.F, (int)(pl.kpad / 32), 1, pl.block_n) : 1;
   // HWCF rows are exactly the GEMM's k order for the im2col (C % 32 == 0: k = tap*C + c) and dense 1x1
   // (k = c) paths, so the GEMM reads W as an MN-major B operand -- no filter_prep launch, no Bt copy
-  pl.b_mn = (pl.a_mode == A_IM2COL || pl.a_mode == A_DENSE) && p.F % 32 == 0 &&
+  pl.b_mn = (pl.a_mode == A_IM2COL || pl.a_mode == A_DENSE || pl.a_mode == A_HALO) && p.F % 32 == 0 &&
             !((variant & 8) && pl.three_x) && getenv("CONV2D_NO_BMN") == nullptr;
   pl.bt_bytes = pl.b_mn ? 0 : round_up((int64_t)pl.npad * pl.kpad * 4, 256);
   pl.pad_bytes = !pl.pad ? 0
@@ -270,7 +270,8 @@ cudaError_t launch_igemm(const Problem& p, bool is_1x1, const float* in, const f
         launch_filter_prep2(filt, p.KH, p.KW, p.C, p.F, pl.cstride, pl.rowstride, pl.kpad, pl.npad, bt_hi, bt_lo, s);
     if (e != cudaSuccess) return e;
   }
-  if (pl.a_mode == A_HALO) return launch_gemm_halo(p, in, bt_hi, bt_lo, pl.kpad, pl.npad, pl.block_n, out, s);
+  if (pl.a_mode == A_HALO)
+    return launch_gemm_halo(p, in, bt_hi, bt_lo, pl.kpad, pl.npad, pl.block_n, out, s, filt, pl.b_mn, pl.three_x);
   Gemm2Args g{};
   g.a_mode = pl.a_mode;
   g.a = in;

@@ -608,7 +608,8 @@ __device__ __forceinline__ void mma2_kblock_tt_concat(uint32_t d, uint32_t ahi_t
 }
 // halo kernel, A (hi | lo) from TMEM, BN = 128: lo x B_hi, hi x B_lo, hi x B_hi
 __device__ __forceinline__ void mma2_kblock_tt_3x(uint32_t d, uint32_t ahi_tmem, uint32_t alo_tmem, uint64_t bx,
-                                                  uint64_t bl, uint32_t idesc, uint32_t acc0) {
+                                                  uint64_t bl, uint32_t idesc, uint32_t acc0, uint32_t b_step = 2) {
+  const uint64_t bs = b_step;  // descriptor units per K=8 step: 2 (K-major SW128), 64 (MN-major, 1 KB)
   asm volatile(
       "{\n\t.reg .pred e, p, t;\n\t.reg .b64 bx, bl;\n\t.reg .b32 ah, al;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
@@ -617,19 +618,19 @@ __device__ __forceinline__ void mma2_kblock_tt_3x(uint32_t d, uint32_t ahi_tmem,
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bx, %5, p;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bl, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bx, %5, t;\n\t"
-      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.u64 bx, bx, 2;\n\tadd.u64 bl, bl, 2;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.u64 bx, bx, %7;\n\tadd.u64 bl, bl, %7;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bx, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bl, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bx, %5, t;\n\t"
-      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.u64 bx, bx, 2;\n\tadd.u64 bl, bl, 2;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.u64 bx, bx, %7;\n\tadd.u64 bl, bl, %7;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bx, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bl, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bx, %5, t;\n\t"
-      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.u64 bx, bx, 2;\n\tadd.u64 bl, bl, 2;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.u64 bx, bx, %7;\n\tadd.u64 bl, bl, %7;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [al], bx, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bl, %5, t;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], [ah], bx, %5, t;\n\t"
-      "}" ::"r"(d), "r"(ahi_tmem), "r"(alo_tmem), "l"(bx), "l"(bl), "r"(idesc), "r"(acc0)
+      "}" ::"r"(d), "r"(ahi_tmem), "r"(alo_tmem), "l"(bx), "l"(bl), "r"(idesc), "r"(acc0), "l"(bs)
       : "memory");
 }
 }  // namespace sm100
