@@ -134,7 +134,8 @@ conv2d_status_t conv2d_set_selected(const conv2d_params_t* p, conv2d_algo_t algo
 
 /* Tuned parameter variant of the implicit_gemm / matmul_1x1 / winograd_f2x2_3x3 kernels for `p` ("different
  * parameters for each algorithm"; the "/variant" of the selection table below).
- * implicit_gemm / matmul_1x1: a bit mask -- A-operand path, N tile, B path, K split (igemm.cu).  Bit 0
+ * implicit_gemm / matmul_1x1: a bit mask -- A-operand path, N tile, B path (bit 3; bit 5 on the 3x3 halo
+ * path in 3xTF32), K split (igemm.cu).  Bit 0
  * (A path) on implicit_gemm: halo <-> im2col for 3x3/s1 with C % 32 == 0; 4-channel halo (0) <-> row-segment
  * boxes (1) for 3x3/s1 with C <= 4 and W*C % 4 == 0; space-to-depth halo <-> row segments for 7x7/s2 stems.
  * winograd_f2x2_3x3: 0 = transform kernels + batched tcgen05 GEMM (winograd.cu), 1 = the fused kernel

@@ -249,12 +249,12 @@ def conv2d_set_variant(p: Params, algo: int, variant: int) -> None:
 
 def conv2d_variants(p: Params, algo: int) -> list:
     """The parameter variants the auto-selector enumerates for (p, algo): exactly those conv2d_set_variant
-    accepts (probes 0..31, restores the recorded variant)."""
+    accepts (probes 0..63, restores the recorded variant)."""
     if algo not in (ALGO_IMPLICIT_GEMM, ALGO_MATMUL_1X1, ALGO_WINOGRAD_F2X2_3X3):
         return [0]
     keep = conv2d_get_variant(p, algo)
     out = []
-    for v in range(32):
+    for v in range(64):
         if _lib.conv2d_set_variant(ctypes.byref(p.c()), int(algo), v) == OK:
             out.append(v)
     conv2d_set_variant(p, algo, keep)

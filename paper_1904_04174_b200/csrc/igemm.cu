@@ -42,7 +42,9 @@ struct Plan {
 // (smem-staged coalesced STG) instead of TMA bulk stores (frees the TMA engine for loads), bit 3 (3xTF32
 // only) routes B through filter_prep's K-major hi/lo copies instead of reading the HWCF filter directly
 // (the direct path saves a launch but splits B's lo halves in smem inside the GEMM: a win for short
-// layers, ~5-8% slower on long tensor-bound ones where smem bandwidth is the limit).
+// layers, ~5-8% slower on long tensor-bound ones where smem bandwidth is the limit), bit 5 (3xTF32, the 3x3
+// halo path, F % 32 == 0) reads the halo path's B straight from the filter too (MN-major boxes + four
+// lo-split warps; in TF32 the halo path always does, no split needed).
 using VKey = std::tuple<int, int, int, int, int, int, int, int, int, int, int, bool>;
 std::mutex g_vmu;
 std::map<VKey, int> g_variant;
@@ -50,7 +52,7 @@ VKey vkey(const Problem& p, bool is_1x1) {
   return VKey(p.N, p.H, p.W, p.C, p.F, p.KH, p.KW, p.SH, p.SW, p.pad_top * 64 + p.pad_left, (int)p.math, is_1x1);
 }
 int variant_of(const Problem& p, bool is_1x1) {
-  if (const char* f = getenv("CONV2D_FORCE_VARIANT")) return atoi(f) & 31;  // parity-test hook
+  if (const char* f = getenv("CONV2D_FORCE_VARIANT")) return atoi(f) & 63;  // parity-test hook
   std::lock_guard<std::mutex> lk(g_vmu);
   auto it = g_variant.find(vkey(p, is_1x1));
   return it == g_variant.end() ? 0 : it->second;
@@ -138,8 +140,11 @@ Plan make_plan(const Problem& p, bool is_1x1, int variant) {
                   ? gemm2_choose_splits(p.M(), p.F, (int)(pl.kpad / 32), 1, pl.block_n) : 1;
   // HWCF rows are exactly the GEMM's k order for the im2col (C % 32 == 0: k = tap*C + c) and dense 1x1
   // (k = c) paths, so the GEMM reads W as an MN-major B operand -- no filter_prep launch, no Bt copy
-  pl.b_mn = (pl.a_mode == A_IM2COL || pl.a_mode == A_DENSE || pl.a_mode == A_HALO) && p.F % 32 == 0 &&
-            !((variant & 8) && pl.three_x) && getenv("CONV2D_NO_BMN") == nullptr;
+  // the halo path reads B straight from the filter always in TF32 and on variant bit 5 in 3xTF32 (there it
+  // needs four lo-split warps and loses on R4 / V2 at b32-b256; it wins at b1 and on R10-like layers)
+  pl.b_mn = (pl.a_mode == A_HALO ? (!pl.three_x || (variant & 32))
+                                 : (pl.a_mode == A_IM2COL || pl.a_mode == A_DENSE) && !((variant & 8) && pl.three_x)) &&
+            p.F % 32 == 0 && getenv("CONV2D_NO_BMN") == nullptr;
   pl.bt_bytes = pl.b_mn ? 0 : round_up((int64_t)pl.npad * pl.kpad * 4, 256);
   pl.pad_bytes = !pl.pad ? 0
                  : rowk ? round_up((int64_t)p.N * pl.hp * pl.wp * pl.cg * 4, 256)
@@ -187,8 +192,11 @@ int igemm_variants(const Problem& p, bool is_1x1, int* masks) {
   int n = 0;
   // bit 0: A path, bit 1: N tile, bit 3: B path.  Bit 2 (LSU-staged epilogue) is not enumerated: it
   // measured slower than TMA stores on every paper layer (reachable through CONV2D_FORCE_VARIANT).
-  for (int m = 0; m < 32; ++m) {
+  // bit 5: the halo path's direct (MN-major) B in 3xTF32 -- only with bit 0 clear (the halo path itself)
+  const bool alt_h = !is_1x1 && p.math == CONV2D_MATH_FP32 && p.F % 32 == 0 && halo_ok(p);
+  for (int m = 0; m < 64; ++m) {
     if (m & 4) continue;
+    if ((m & 32) && (!alt_h || (m & 1) || (m & 8))) continue;
     if ((m & 1) && !alt_a) continue;
     if ((m & 2) && !alt_n) continue;
     if ((m & 8) && !alt_b) continue;

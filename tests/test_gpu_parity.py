@@ -365,7 +365,7 @@ def test_tf32_mma_reads_truncated_operands(cuda_ok):
     assert np.array_equal(gpu_conv(p, x, w, a), gpu_conv(p, xt, wt, a))
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 7, 8, 11, 16, 17, 18, 24])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 7, 8, 11, 16, 17, 18, 24, 32, 34])
 @pytest.mark.parametrize("case", [(2, 28, 28, 64, 64, 3, 3, 1, 1, 0), (1, 14, 15, 128, 128, 3, 3, 1, 1, 1),
                                   (2, 12, 12, 64, 256, 1, 1, 1, 1, 0), (1, 9, 9, 64, 320, 3, 3, 2, 2, 0),
                                   (2, 21, 19, 3, 36, 7, 7, 2, 2, 0),

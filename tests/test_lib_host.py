@@ -166,7 +166,13 @@ def test_variant_get_set_host_side(C):
     assert C.conv2d_get_variant(p, C.ALGO_IMPLICIT_GEMM) == 1
     C.conv2d_set_variant(p, C.ALGO_IMPLICIT_GEMM, 0)
     assert C.conv2d_get_variant(p, C.ALGO_IMPLICIT_GEMM) == 0
-    for bad in (4, 32, -1):  # bit 2 (LSU epilogue) is never enumerated; out of range
+    # bit 5 (the halo path's direct B in 3xTF32) is enumerated here, with bit 0 clear only
+    C.conv2d_set_variant(p, C.ALGO_IMPLICIT_GEMM, 32)
+    assert C.conv2d_get_variant(p, C.ALGO_IMPLICIT_GEMM) == 32
+    assert 32 in C.conv2d_variants(p, C.ALGO_IMPLICIT_GEMM) and 33 not in C.conv2d_variants(p, C.ALGO_IMPLICIT_GEMM)
+    assert 32 not in C.conv2d_variants(p.replace(math=C.MATH_TF32), C.ALGO_IMPLICIT_GEMM)  # TF32: always direct
+    # bit 2 (LSU epilogue) is never enumerated; bit 5 with bit 0 (im2col path); out of range
+    for bad in (4, 33, 64, -1):
         with pytest.raises(C.Conv2dError) as e:
             C.conv2d_set_variant(p, C.ALGO_IMPLICIT_GEMM, bad)
         assert e.value.status == C.ERR_INVALID_PARAMS
