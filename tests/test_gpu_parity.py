@@ -374,6 +374,8 @@ def test_tf32_mma_reads_truncated_operands(cuda_ok):
                                   # remainder split: 150 / 85 / 100 pair tiles (last wave 2 / 11 / 26 of 74)
                                   (2, 150, 128, 256, 64, 1, 1, 1, 1, 0), (5, 68, 64, 96, 128, 3, 3, 1, 1, 0),
                                   (8, 28, 28, 256, 1024, 1, 1, 1, 1, 0),
+                                  # 3x3 halo, F = 96 (a partly out-of-range 32-column chunk of the direct-B boxes)
+                                  (2, 12, 12, 32, 96, 3, 3, 1, 1, 0),
                                   # balanced K split: 40 pair tiles of 32 k-blocks (74 / 40 = 1 -> modelled best 3)
                                   (10, 32, 32, 1024, 64, 1, 1, 1, 1, 0)], ids=str)
 def test_algorithm_parameter_variants(cuda_ok, monkeypatch, variant, case):
@@ -401,6 +403,7 @@ C4_CASES = [  # (N, H, W, C, F, KH, KW, SH, SW, pad): 3x3 / s1, C <= 4, W*C % 4 
     (1, 9, 6, 2, 40, 3, 3, 1, 1, 0),       # C = 2, one tile
     (2, 33, 29, 4, 128, 3, 3, 1, 1, 0),    # C = 4 (no zero slots), BN = 128
     (1, 40, 36, 3, 200, 3, 3, 1, 1, 1),    # F > 128: two N tiles
+    (1, 31, 40, 3, 96, 3, 3, 1, 1, 0),     # F = 96: BN = 128 with a zero column block
 ]
 
 
