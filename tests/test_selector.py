@@ -20,7 +20,8 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "paper_1904_04174_b200", "csrc", "selector_tree.h")
 DATA = [os.path.join(ROOT, "profiles", "data", f)
-        for f in ("selector_data_r1.json", "selector_data_r1b.json", "selector_data_r1c.json", "selector_data_r1d.json.gz")]
+        for f in ("selector_data_r1.json", "selector_data_r1b.json", "selector_data_r1c.json", "selector_data_r1d.json.gz",
+                  "selector_data_r2_c4.json")]  # r2_c4: the C <= 4 3x3 shapes re-timed on the 4-channel halo path
 
 
 @pytest.fixture(scope="module")

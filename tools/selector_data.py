@@ -4,6 +4,11 @@ decisions involve many parameters and a large number of features ... a good cand
 solution rather than a hand tuned one").
 
     python tools/selector_data.py --shapes 400 --seed 3 --out gpurun_out/selector_data.json
+    python tools/selector_data.py --replay profiles/data/selector_data_r1*.json --only c4 --out ...
+
+(--replay re-times the shapes of earlier data files -- filtered by --only -- with the current library: a
+round-2 path change, e.g. the 4-channel halo of 3x3/s1 C <= 4 layers, changes what a candidate means there, and
+tools/train_selector.py lets the later file's rows replace the earlier ones.)
 
 For every conv shape -- the paper's 35 layer tuples at batch 1 / 32 / 256 in both math modes, then random
 CNN-like shapes (window 1/3/5/7, stride 1/2, 7..224 pixels, 3..2048 channels, batch 1..256, bounded work) --
@@ -86,6 +91,9 @@ def main():
     ap.add_argument("--shapes", type=int, default=400)
     ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--out", default="gpurun_out/selector_data.json")
+    ap.add_argument("--replay", nargs="*", default=[], help="re-time the shapes of these data files instead")
+    ap.add_argument("--only", choices=["all", "c4"], default="all",
+                    help="c4: only 3x3 / stride 1 shapes with C <= 4, W*C % 4 == 0, F <= 128 (A_C4-eligible)")
     args = ap.parse_args()
 
     import torch
@@ -94,7 +102,18 @@ def main():
     torch.cuda.set_device(0)
     FLUSH[0] = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     rng = np.random.default_rng(args.seed)
-    shapes = paper_shapes() + random_shapes(args.shapes, rng)
+    if args.replay:
+        import gzip
+        shapes = []
+        for path in args.replay:
+            fh = gzip.open(path, "rt") if path.endswith(".gz") else open(path)
+            shapes += [r["params"] for r in json.load(fh)["rows"]]
+    else:
+        shapes = paper_shapes() + random_shapes(args.shapes, rng)
+    if args.only == "c4":
+        shapes = [sp for sp in shapes if sp["window_rows"] == 3 and sp["window_cols"] == 3 and sp["stride_rows"] == 1
+                  and sp["stride_cols"] == 1 and sp["channels"] <= 4 and (sp["in_cols"] * sp["channels"]) % 4 == 0
+                  and sp["features"] <= 128]
     rows = []
     for i, sp in enumerate(shapes):
         p = C.Params(**sp)
@@ -113,7 +132,7 @@ def main():
             variants = [None]
             if a in (C.ALGO_IMPLICIT_GEMM, C.ALGO_MATMUL_1X1):
                 variants = []
-                for v in range(32):  # the enumerated variants are exactly those set_variant accepts
+                for v in range(64):  # the enumerated variants are exactly those set_variant accepts
                     try:
                         C.conv2d_set_variant(p, a, v)
                         variants.append(v)
@@ -128,7 +147,10 @@ def main():
         print(f"{i:4d} {sp} -> {best}  {times[best]:.1f} us ({len(times)} candidates)", flush=True)
         del x, w, y, ws
     with open(args.out, "w") as fh:
-        json.dump({"device": torch.cuda.get_device_name(0), "rows": rows}, fh)
+        out = {"device": torch.cuda.get_device_name(0), "rows": rows}
+        if args.replay and args.only != "all":
+            out["supersedes"] = args.only  # tools/train_selector.py drops the earlier rows of this class
+        json.dump(out, fh)
 
 
 if __name__ == "__main__":

@@ -51,12 +51,28 @@ def features(sp):
             math.log2(ho * wo), sp["math"], math.log2(tiles), math.log2(flops), flops / nbytes]
 
 
+def c4_eligible(sp):
+    """3x3 / stride 1, C <= 4, W*C % 4 == 0, F <= 128: the shapes round 2's 4-channel halo path took over."""
+    return (sp["window_rows"] == 3 and sp["window_cols"] == 3 and sp["stride_rows"] == 1 and sp["stride_cols"] == 1
+            and sp["channels"] <= 4 and (sp["in_cols"] * sp["channels"]) % 4 == 0 and sp["features"] <= 128)
+
+
+SUPERSEDE = {"c4": c4_eligible}
+
+
 def load(paths):
+    """Rows of every data file, in order.  A file whose top level carries "supersedes": <class> (a re-timing of
+    the shapes whose candidates changed meaning, tools/selector_data.py --replay --only <class>) first drops the
+    earlier rows of that class."""
     import gzip
     rows = []
     for p in paths:
         with (gzip.open(p, "rt") if p.endswith(".gz") else open(p)) as fh:
-            rows += json.load(fh)["rows"]
+            d = json.load(fh)
+        if d.get("supersedes"):
+            keep = SUPERSEDE[d["supersedes"]]
+            rows = [r for r in rows if not keep(r["params"])]
+        rows += d["rows"]
     return rows
 
 
